@@ -1,0 +1,194 @@
+/*
+ * rbf_b200.h -- C ABI of the B200 (sm_100a) hot path for GCB-greedy RBF mesh
+ * deformation (Fang et al., arXiv 2004.04817).
+ *
+ * The reference (`rbfdeform`, pure Python) has no FFI layer: its only
+ * interface is the Python API. Each entry point below replaces the
+ * reference function named beside it; the Python package
+ * `paper_2004_04817_b200` binds them with ctypes and keeps the reference's
+ * names, argument meaning and exceptions.
+ *
+ * Conventions
+ *  - Every pointer argument is a DEVICE pointer (caller-owned, e.g. torch
+ *    tensors) unless its name ends in `_host`. Arrays of points,
+ *    displacements and weights are C-contiguous (n, 3) float64 (AoS), the
+ *    reference's layout (core.py:227-265, selection.py:46-83).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream). Calls are
+ *    stream-ordered and asynchronous unless documented otherwise.
+ *  - The library never allocates or frees caller memory; scratch buffers
+ *    are passed in and sized by rbf_*_scratch_bytes().
+ *  - Return value: RBF_OK or an RBF_E* code; rbf_last_error() gives a
+ *    thread-local message. No CPU fallback exists: without a CUDA device
+ *    every compute entry point returns RBF_ECUDA.
+ */
+#ifndef RBF_B200_H
+#define RBF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define RBF_API __attribute__((visibility("default")))
+#else
+#define RBF_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RBF_ABI_VERSION 1
+
+enum {
+  RBF_OK = 0,
+  RBF_EARG = 1,     /* bad argument -> ValueError family                    */
+  RBF_ECUDA = 2,    /* CUDA runtime error / no device                       */
+  RBF_ENOTPD = 3,   /* NotPositiveDefiniteError (errors.py:13-15)            */
+  RBF_EGROW = 5,    /* selection loop paused: factor/record capacity full    */
+  RBF_ESTALL = 6,   /* SelectionStalledError (errors.py:44-46)               */
+  RBF_ENCCL = 4     /* reserved: collective error                            */
+};
+
+RBF_API int rbf_abi_version(void);
+RBF_API const char* rbf_last_error(void);
+/* Number of SMs and cooperative CTAs the selection loop uses on `device`. */
+RBF_API int rbf_device_info(int device, int* sm_count_host, int* loop_ctas_host);
+
+/* ---------------------------------------------------------------------
+ * Volume / boundary evaluation.
+ * Replaces core.py:301-334 `_eval_displacements` (called by
+ * evaluate_displacements core.py:337-351, evaluate_displacement
+ * core.py:354-356 and deform_points core.py:359-367):
+ *   out[k] = sum_i w_i * phi(|p_k - s_i| / radius)          (deform == 0)
+ *   out[k] = p_k + sum_i w_i * phi(|p_k - s_i| / radius)    (deform == 1)
+ * The per-target summation order is fixed (independent of n_targets and of
+ * how targets are sharded), so shards are bitwise identical to a single
+ * call. `out` may not alias `targets`.
+ */
+RBF_API int rbf_eval(const double* targets, int64_t n_targets,
+             const double* sup_points, const double* sup_weights, int64_t n_sup,
+             double radius, int deform, double* out, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Interpolation error at boundary rows, fused with the (err, lowest id)
+ * arg-max.  Replaces selection.py:215-221 `_errors_at` +
+ * selection.py:231-234 `_argmax_lowest_id` (as used by
+ * group_arg_max_error selection.py:237-254 and the final sweep
+ * selection.py:394-402):
+ *   err[t] = | disp[pos[t]] - sum_i w_i phi(|pts[pos[t]] - s_i| / R) |_2
+ * `positions` may be NULL (then pos[t] = t). `err_out` may be NULL.
+ * `best_host` (may be NULL) receives {max_err, (double)pos_of_max} after a
+ * stream synchronisation; ties go to the lowest position.
+ * `scratch` must hold rbf_errors_scratch_bytes(n_targets) bytes.
+ */
+RBF_API size_t rbf_errors_scratch_bytes(int64_t n_targets);
+RBF_API int rbf_errors_argmax(const double* bnd_points, const double* bnd_disp,
+                      const int64_t* positions, int64_t n_targets,
+                      const double* sup_points, const double* sup_weights, int64_t n_sup,
+                      double radius, double* err_out, double* best_host,
+                      void* scratch, size_t scratch_bytes, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Growing Cholesky factor.  Replaces core.py:115-205 `CholeskyState`.
+ * The factor L and its inverse Li are stored as PACKED lower triangles,
+ * row-major (row i starts at i*(i+1)/2), so capacity growth is a prefix
+ * copy. `n` is the current order.
+ *
+ * rbf_chol_append (core.py:153-185): given row[0..n] (the new matrix row
+ * against the n prior indices plus itself), computes c = L^-1 row[:n]
+ * (inverse product plus one step of residual refinement) and
+ * pivot^2 = row[n] - c.c. If pivot^2 > 0 it writes row n of L and Li and
+ * returns RBF_OK; otherwise it returns RBF_ENOTPD and leaves the state
+ * unchanged. `pivot2_host` receives pivot^2 in both cases. Synchronous.
+ * L and Li must have room for (n+1)(n+2)/2 doubles. `scratch` holds
+ * rbf_chol_scratch_bytes(n+1) bytes.
+ */
+RBF_API size_t rbf_chol_scratch_bytes(int64_t n);
+RBF_API int rbf_chol_append(double* L, double* Li, int64_t n, const double* row,
+                    double* pivot2_host, void* scratch, size_t scratch_bytes,
+                    void* stream);
+
+/* rbf_chol_solve (core.py:187-205): x = (L L^T)^-1 rhs for rhs (n, k)
+ * row-major, k >= 1. out may alias rhs. */
+RBF_API int rbf_chol_solve(const double* L, const double* Li, int64_t n,
+                   const double* rhs, int64_t k, double* out,
+                   void* scratch, size_t scratch_bytes, void* stream);
+
+/* ---------------------------------------------------------------------
+ * The GCB / greedy selection loop, fully device resident.
+ * Replaces selection.py:274-421 `_gcb_run` (entry points gcb_select
+ * selection.py:257-271 and greedy_select selection.py:424-428).
+ *
+ * The host does what must stay bit-identical to numpy: the PCG64
+ * partition (selection.py:177-185) and the three seeds
+ * (selection.py:198-212); it passes them in. One cooperative persistent
+ * kernel then runs seeding appends, every iteration (weights update,
+ * group scan + arg-max, candidate walk with near-duplicate and pivot
+ * rejection, factor append), the termination logic and the final sweep.
+ * It returns RBF_EGROW when the factor or record buffers are full: the host
+ * grows them (packed prefixes are capacity independent) and calls again
+ * with the same state, which resumes the same iteration.
+ */
+typedef struct rbf_gcb_record {
+  int32_t group;      /* group visited (-1 for the final sweep)             */
+  int32_t node_pos;   /* position of the added node, else of the arg-max   */
+  int32_t added;      /* 1 if a node was appended this iteration           */
+  int32_t n_before;   /* support count during the scan                     */
+  double local_max;   /* max error in the group (ineligible nodes included) */
+  double t1_s;        /* scan time (device clock)                          */
+  double t2_s;        /* factor/weights time carried into this record      */
+} rbf_gcb_record;
+
+typedef struct rbf_gcb_state {
+  int32_t n;            /* current support count                          */
+  int32_t k;            /* iteration counter (starts at 3, selection.py:307) */
+  int32_t streak_ok;    /* selection.py:373-386                            */
+  int32_t streak_noadd;
+  int32_t n_records;
+  int32_t status;       /* 0 running, 1 done, RBF_E* on failure            */
+  int32_t fail_row;     /* NotPD: row index of the failing seed append     */
+  int32_t done_loop;    /* 1 once the loop ended (final sweep pending/done) */
+  double fail_pivot2;
+  double t2_carry;
+  double final_max;     /* final sweep */
+  int32_t final_pos;
+  int32_t fault;        /* watchdog flag                                   */
+} rbf_gcb_state;
+
+typedef struct rbf_gcb_args {
+  /* boundary (device) */
+  const double* points;     /* (nb, 3) */
+  const double* disp;       /* (nb, 3) */
+  const int32_t* group_pos; /* (nb) positions, groups concatenated        */
+  const int32_t* group_off; /* (m + 1) offsets into group_pos              */
+  int32_t nb, m;
+  int32_t seeds[3];         /* seed positions (host computed)             */
+  int32_t max_supports;
+  double radius, tol;
+  double dup_dist;          /* NEAR_DUPLICATE_FRACTION * radius            */
+  /* factor state (device), capacity in rows */
+  double* L;                /* packed, cap*(cap+1)/2 */
+  double* Li;               /* packed, cap*(cap+1)/2 */
+  double* y;                /* (cap, 3) forward-substituted displacements */
+  double* sup;              /* (cap, 8) scaled x,y,z, weights wx,wy,wz, 2 pad */
+  int32_t* sel;             /* (cap) selected positions in order          */
+  uint8_t* inel;            /* (nb) ineligible flags                       */
+  int32_t cap;
+  /* records (device) */
+  rbf_gcb_record* records;
+  int32_t rec_cap;
+  /* state + scratch (device) */
+  rbf_gcb_state* state;
+  void* scratch;            /* rbf_gcb_scratch_bytes(nb, cap, ctas) bytes */
+  size_t scratch_bytes;
+} rbf_gcb_args;
+
+RBF_API size_t rbf_gcb_scratch_bytes(int32_t nb, int32_t cap, int32_t ctas);
+/* Launch (asynchronous). The caller zero-initialises *state (n = 0) and
+ * inel before the first call. */
+RBF_API int rbf_gcb_run(const rbf_gcb_args* args, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RBF_B200_H */

@@ -1,0 +1,184 @@
+// Shared device helpers for the B200 RBF hot path (sm_100a, FP64 CUDA cores).
+//
+// Two evaluations of the Wendland C2 kernel live here:
+//  * phi_exact(): the reference's per-element chain with every operation
+//    rounded separately (no FMA contraction), used for Cholesky rows so the
+//    factored matrix is bit-identical to the reference's
+//    (reference: core.py:45-50 `_phi`, selection.py:289-295 / 342-347 the
+//    row `[phi(cdist/R)..., 1.0]`; cdist is sqrt((dx*dx+dy*dy)+dz*dz)).
+//  * pair_accum(): the throughput path for the error scan and volume
+//    evaluation (reference: core.py:316-326 `_eval_displacements` inner
+//    tile), coordinates pre-scaled by 1/R so eta = |p - s| directly.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rbf {
+
+constexpr int kWarp = 32;
+
+// ---------------------------------------------------------------- numerics
+__device__ __forceinline__ double cdist_exact(double ax, double ay, double az,
+                                              double bx, double by, double bz) {
+  double dx = __dsub_rn(ax, bx), dy = __dsub_rn(ay, by), dz = __dsub_rn(az, bz);
+  return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                              __dmul_rn(dz, dz)));
+}
+
+// reference core.py:45-50 with eta = d / R (numpy true division)
+__device__ __forceinline__ double phi_exact(double d, double radius) {
+  double eta = __ddiv_rn(d, radius);
+  double t = fmax(__dsub_rn(1.0, eta), 0.0);
+  t = __dmul_rn(t, t);
+  t = __dmul_rn(t, t);
+  return __dmul_rn(t, __dadd_rn(__dmul_rn(4.0, eta), 1.0));
+}
+
+__device__ __forceinline__ double rsqrt_approx(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
+// max(t, +0) through the sign bit: integer ops only, keeps the FP64 pipe free
+__device__ __forceinline__ double clamp_nonneg(double t) {
+  const int hi = __double2hiint(t), lo = __double2loint(t);
+  const int keep = ~(hi >> 31);
+  return __hiloint2double(hi & keep, lo & keep);
+}
+
+// Throughput pair: target (px,py,pz) and support (sx,sy,sz) already scaled
+// by 1/R; accumulates w * phi(|p - s|) into (ax, ay, az).
+//
+// FP64-pipe budget per pair: 3 DADD (differences) + 3 (r^2) + 5 (rsqrt
+// refinement) + 2 (t = 1 - r2*y, q = 5 - 4t = 4 eta + 1) + 3 (t^2, t^4,
+// t^4 q) + 3 DFMA (accumulate) = 19. eta = sqrt(r2) is never formed:
+// y = rsqrt(r2) comes from MUFU.RSQ64H plus one third-order correction
+// (relative error ~2^-60), t = fma(-r2, y, 1). r2 below 1e-200 is lifted to
+// 1e-200 (eta = 1e-100 gives phi = 1 exactly, like eta = 0) so the rsqrt
+// never sees zero. The clamp t = max(t, 0) is integer-only.
+__device__ __forceinline__ void pair_accum(double px, double py, double pz,
+                                           double sx, double sy, double sz,
+                                           double wx, double wy, double wz,
+                                           double& ax, double& ay, double& az) {
+  const double dx = px - sx, dy = py - sy, dz = pz - sz;
+  double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+  const int kTinyHi = 0x16687e92;  // high word of 1e-200
+  const int hi = __double2hiint(r2);
+  r2 = __hiloint2double(max(hi, kTinyHi), __double2loint(r2));
+  const double y0 = rsqrt_approx(r2);
+  const double e = fma(-r2, y0 * y0, 1.0);
+  const double p = fma(e, 0.375, 0.5);
+  const double y = fma(p, y0 * e, y0);
+  double t = clamp_nonneg(fma(-r2, y, 1.0));
+  const double q = fma(-4.0, t, 5.0);
+  t = t * t;
+  const double f = (t * t) * q;
+  ax = fma(wx, f, ax);
+  ay = fma(wy, f, ay);
+  az = fma(wz, f, az);
+}
+
+// residual norm exactly as selection.py:220-221: sqrt((r0*r0 + r1*r1) + r2*r2)
+__device__ __forceinline__ double residual_norm(double dx, double dy, double dz,
+                                                double ux, double uy, double uz) {
+  double r0 = __dsub_rn(dx, ux), r1 = __dsub_rn(dy, uy), r2 = __dsub_rn(dz, uz);
+  return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1)),
+                              __dmul_rn(r2, r2)));
+}
+
+// ------------------------------------------------------- (err, pos) argmax
+// Larger error wins; exact ties go to the lowest position (= lowest id, since
+// boundary indices are strictly increasing: selection.py:46-52, 231-234).
+struct Best {
+  double err;
+  int pos;
+};
+
+__device__ __forceinline__ bool better(double e1, int p1, double e2, int p2) {
+  return e1 > e2 || (e1 == e2 && p1 < p2);
+}
+
+__device__ __forceinline__ Best best_of(Best a, Best b) {
+  return better(b.err, b.pos, a.err, a.pos) ? b : a;
+}
+
+__device__ __forceinline__ Best warp_best(Best b) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    double e = __shfl_xor_sync(0xffffffffu, b.err, off);
+    int p = __shfl_xor_sync(0xffffffffu, b.pos, off);
+    if (better(e, p, b.err, b.pos)) {
+      b.err = e;
+      b.pos = p;
+    }
+  }
+  return b;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, off));
+  return v;
+}
+
+// ---------------------------------------------------------- memory helpers
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ int ldcg(const int* p) { return __ldcg(p); }
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ------------------------------------------------------------ grid barrier
+// Sense-counting barrier for a cooperative (co-resident) grid. A spin that
+// exceeds the watchdog sets *fault and traps instead of hanging the GPU.
+struct GridBarrier {
+  unsigned count;
+  unsigned gen;
+};
+
+__device__ __forceinline__ void grid_sync(GridBarrier* bar, unsigned nblocks, int* fault) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned g = ld_acquire(&bar->gen);
+    __threadfence();
+    unsigned prev = atomicAdd(&bar->count, 1u);
+    if (prev == nblocks - 1) {
+      bar->count = 0;
+      __threadfence();
+      st_release(&bar->gen, g + 1);
+    } else {
+      uint64_t t0 = globaltimer_ns();
+      unsigned spins = 0;
+      while (ld_acquire(&bar->gen) == g) {
+        if ((++spins & 1023u) == 0 && globaltimer_ns() - t0 > 20ull * 1000000000ull) {
+          atomicExch(fault, 1);
+          __trap();
+        }
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+}  // namespace rbf

@@ -1,0 +1,188 @@
+// Volume evaluation and boundary error scan (throughput kernels).
+//
+// Replaces reference core.py:301-334 `_eval_displacements` (2048-row spans x
+// 512-column tiles on a CPU thread pool, supports padded to a tile multiple
+// by core.py:284-298) with one CUDA grid: every thread owns TPT targets in
+// registers, support tiles (coordinates pre-scaled by 1/R, weights) are
+// staged through shared memory and read as warp-wide broadcasts, partial
+// tiles are handled by the loop bound (no padding sentinels). The summation
+// order per target is support order, independent of the launch geometry, so
+// any sharding of the targets reproduces single-GPU results bit for bit.
+#include <cstdint>
+
+#include "rbf_common.cuh"
+#include "rbf_internal.h"
+
+namespace rbf {
+
+constexpr int kEvalThreads = 128;
+constexpr int kEvalTPT = 4;
+constexpr int kEvalTile = 128;
+constexpr int kEvalTargetsPerBlock = kEvalThreads * kEvalTPT;
+
+enum EvalMode { kModeEval = 0, kModeDeform = 1, kModeError = 2 };
+
+template <int MODE>
+__global__ void __launch_bounds__(kEvalThreads, 4)
+eval_kernel(const double* __restrict__ tpts, const double* __restrict__ tdisp,
+            const int64_t* __restrict__ pos, int64_t nt,
+            const double* __restrict__ spts, const double* __restrict__ sw, int nsup,
+            double inv_r, double* __restrict__ out, Best* __restrict__ partials) {
+  __shared__ double4 s_a[kEvalTile];  // scaled x, y, z, wx
+  __shared__ double2 s_b[kEvalTile];  // wy, wz
+
+  const int64_t base = (int64_t)blockIdx.x * kEvalTargetsPerBlock + threadIdx.x;
+  double px[kEvalTPT], py[kEvalTPT], pz[kEvalTPT];
+  double ax[kEvalTPT], ay[kEvalTPT], az[kEvalTPT];
+  int64_t row[kEvalTPT];
+#pragma unroll
+  for (int k = 0; k < kEvalTPT; ++k) {
+    int64_t idx = base + (int64_t)k * kEvalThreads;
+    int64_t r = -1;
+    if (idx < nt) r = (MODE == kModeError && pos) ? pos[idx] : idx;
+    row[k] = r;
+    if (r >= 0) {
+      px[k] = tpts[3 * r] * inv_r;
+      py[k] = tpts[3 * r + 1] * inv_r;
+      pz[k] = tpts[3 * r + 2] * inv_r;
+    } else {
+      px[k] = py[k] = pz[k] = 0.0;
+    }
+    ax[k] = ay[k] = az[k] = 0.0;
+  }
+
+  for (int t0 = 0; t0 < nsup; t0 += kEvalTile) {
+    const int cnt = min(kEvalTile, nsup - t0);
+    __syncthreads();
+    for (int j = threadIdx.x; j < cnt; j += kEvalThreads) {
+      const int g = t0 + j;
+      s_a[j] = make_double4(spts[3 * g] * inv_r, spts[3 * g + 1] * inv_r,
+                            spts[3 * g + 2] * inv_r, sw[3 * g]);
+      s_b[j] = make_double2(sw[3 * g + 1], sw[3 * g + 2]);
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int j = 0; j < cnt; ++j) {
+      const double4 a = s_a[j];
+      const double2 b = s_b[j];
+#pragma unroll
+      for (int k = 0; k < kEvalTPT; ++k)
+        pair_accum(px[k], py[k], pz[k], a.x, a.y, a.z, a.w, b.x, b.y, ax[k], ay[k], az[k]);
+    }
+  }
+
+  if (MODE == kModeError) {
+    Best best{-1.0, 0x7fffffff};
+#pragma unroll
+    for (int k = 0; k < kEvalTPT; ++k) {
+      const int64_t r = row[k];
+      if (r < 0) continue;
+      const double e = residual_norm(tdisp[3 * r], tdisp[3 * r + 1], tdisp[3 * r + 2],
+                                     ax[k], ay[k], az[k]);
+      if (out) out[base + (int64_t)k * kEvalThreads] = e;
+      if (better(e, (int)r, best.err, best.pos)) best = Best{e, (int)r};
+    }
+    best = warp_best(best);
+    __shared__ Best s_best[kEvalThreads / kWarp];
+    if ((threadIdx.x & 31) == 0) s_best[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Best b = s_best[0];
+      for (int w = 1; w < kEvalThreads / kWarp; ++w) b = best_of(b, s_best[w]);
+      partials[blockIdx.x] = b;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kEvalTPT; ++k) {
+      const int64_t r = row[k];
+      if (r < 0) continue;
+      if (MODE == kModeDeform) {
+        out[3 * r] = tpts[3 * r] + ax[k];
+        out[3 * r + 1] = tpts[3 * r + 1] + ay[k];
+        out[3 * r + 2] = tpts[3 * r + 2] + az[k];
+      } else {
+        out[3 * r] = ax[k];
+        out[3 * r + 1] = ay[k];
+        out[3 * r + 2] = az[k];
+      }
+    }
+  }
+}
+
+// One block folds the per-block (err, pos) partials in block order.
+__global__ void best_reduce_kernel(const Best* __restrict__ partials, int n, double* __restrict__ result) {
+  Best b{-1.0, 0x7fffffff};
+  for (int i = threadIdx.x; i < n; i += blockDim.x) b = best_of(b, partials[i]);
+  b = warp_best(b);
+  __shared__ Best s[32];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Best r = s[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = best_of(r, s[w]);
+    result[0] = r.err;
+    result[1] = (double)r.pos;
+  }
+}
+
+static inline int64_t eval_blocks(int64_t nt) {
+  return (nt + kEvalTargetsPerBlock - 1) / kEvalTargetsPerBlock;
+}
+
+}  // namespace rbf
+
+using namespace rbf;
+
+extern "C" int rbf_eval(const double* targets, int64_t n_targets, const double* sup_points,
+                        const double* sup_weights, int64_t n_sup, double radius, int deform,
+                        double* out, void* stream) {
+  if (n_targets < 0 || n_sup < 0) return set_error(RBF_EARG, "negative size");
+  if (!(radius > 0.0)) return set_error(RBF_EARG, "radius must be positive, got %g", radius);
+  if (n_sup > INT32_MAX) return set_error(RBF_EARG, "too many supports");
+  if (n_targets == 0) return RBF_OK;
+  if (!targets || !out || (n_sup > 0 && (!sup_points || !sup_weights)))
+    return set_error(RBF_EARG, "null pointer");
+  const int64_t nblk = eval_blocks(n_targets);
+  const double inv_r = 1.0 / radius;
+  cudaStream_t s = as_stream(stream);
+  if (deform)
+    eval_kernel<kModeDeform><<<(unsigned)nblk, kEvalThreads, 0, s>>>(
+        targets, nullptr, nullptr, n_targets, sup_points, sup_weights, (int)n_sup, inv_r, out, nullptr);
+  else
+    eval_kernel<kModeEval><<<(unsigned)nblk, kEvalThreads, 0, s>>>(
+        targets, nullptr, nullptr, n_targets, sup_points, sup_weights, (int)n_sup, inv_r, out, nullptr);
+  RBF_LAUNCH_CHECK("eval_kernel");
+  return RBF_OK;
+}
+
+extern "C" size_t rbf_errors_scratch_bytes(int64_t n_targets) {
+  return 256 + (size_t)eval_blocks(n_targets < 1 ? 1 : n_targets) * sizeof(Best);
+}
+
+extern "C" int rbf_errors_argmax(const double* bnd_points, const double* bnd_disp,
+                                 const int64_t* positions, int64_t n_targets,
+                                 const double* sup_points, const double* sup_weights, int64_t n_sup,
+                                 double radius, double* err_out, double* best_host, void* scratch,
+                                 size_t scratch_bytes, void* stream) {
+  if (n_targets <= 0) return set_error(RBF_EARG, "group is empty");
+  if (!(radius > 0.0)) return set_error(RBF_EARG, "radius must be positive, got %g", radius);
+  if (n_sup > INT32_MAX || n_targets > INT32_MAX) return set_error(RBF_EARG, "size too large");
+  if (!bnd_points || !bnd_disp || !scratch) return set_error(RBF_EARG, "null pointer");
+  if (scratch_bytes < rbf_errors_scratch_bytes(n_targets))
+    return set_error(RBF_EARG, "scratch too small");
+  const int64_t nblk = eval_blocks(n_targets);
+  cudaStream_t s = as_stream(stream);
+  double* result = reinterpret_cast<double*>(scratch);
+  Best* partials = reinterpret_cast<Best*>(static_cast<char*>(scratch) + 256);
+  eval_kernel<kModeError><<<(unsigned)nblk, kEvalThreads, 0, s>>>(
+      bnd_points, bnd_disp, positions, n_targets, sup_points, sup_weights, (int)n_sup,
+      1.0 / radius, err_out, partials);
+  RBF_LAUNCH_CHECK("eval_kernel<error>");
+  best_reduce_kernel<<<1, 256, 0, s>>>(partials, (int)nblk, result);
+  RBF_LAUNCH_CHECK("best_reduce_kernel");
+  if (best_host) {
+    RBF_CUDA_TRY(cudaMemcpyAsync(best_host, result, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  return RBF_OK;
+}

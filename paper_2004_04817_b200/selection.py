@@ -1,0 +1,450 @@
+"""Support-node selection (greedy and grouped-circular greedy) on the B200.
+
+Drop-in mirror of reference ``selection.py``. The data types, the seeded
+PCG64 partition (selection.py:177-185) and the seeds (selection.py:198-212)
+stay numpy so they are bit-identical to the reference; the whole selection
+loop (``_gcb_run``, selection.py:274-421) runs as ONE cooperative
+persistent kernel of the sm_100a library (``rbf_gcb_run``,
+csrc/rbf_gcb.cu). The host reads the support set, weights and
+per-iteration records back once, at the end.
+
+Timings in the records come from the device clock (%globaltimer) around
+the same stages the reference brackets with ``perf_counter``: t1 = group
+scan, t2 = weights update + candidate appends (carried into the next
+record, selection.py:310-316, 357).
+"""
+
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from . import _native as N
+from .core import (
+    SupportSet,
+    _device,
+    _to_device,
+    _to_host,
+    _tri,
+    evaluate_displacement,
+    solve_support_weights,
+)
+from .errors import (
+    EmptyGroupError,
+    InvalidCountError,
+    InvalidGroupCountError,
+    NotPositiveDefiniteError,
+    SelectionStalledError,
+    TooFewBoundaryNodesError,
+    UnknownIndexError,
+)
+
+# reference selection.py:43
+NEAR_DUPLICATE_FRACTION = 1e-12
+
+
+@dataclass(eq=False)
+class BoundarySet:
+    """Boundary nodes with prescribed displacements (selection.py:46-83)."""
+
+    indices: np.ndarray
+    points: np.ndarray
+    disp: np.ndarray
+
+    def __post_init__(self):
+        self.indices = np.asarray(self.indices, dtype=np.intp)
+        self.points = np.asarray(self.points, dtype=float)
+        self.disp = np.asarray(self.disp, dtype=float)
+        nb = len(self.indices)
+        if nb == 0:
+            raise ValueError("boundary set is empty")
+        if self.points.shape != (nb, 3) or self.disp.shape != (nb, 3):
+            raise ValueError(
+                f"points {self.points.shape} and disp {self.disp.shape} must both be ({nb}, 3)"
+            )
+        if nb > 1 and not (np.diff(self.indices) > 0).all():
+            raise ValueError("boundary indices must be strictly increasing")
+        if not np.isfinite(self.points).all() or not np.isfinite(self.disp).all():
+            raise ValueError("boundary points and displacements must be finite")
+
+    def __len__(self):
+        return len(self.indices)
+
+    def position_of(self, index):
+        pos = int(np.searchsorted(self.indices, index))
+        if pos == len(self.indices) or self.indices[pos] != index:
+            raise UnknownIndexError(f"{index} is not a boundary node")
+        return pos
+
+
+@dataclass(eq=False)
+class GroupPartition:
+    """m disjoint balanced groups of boundary ids (selection.py:86-102)."""
+
+    m: int
+    groups: list
+    seed: int
+
+    def __post_init__(self):
+        sizes = [len(g) for g in self.groups]
+        if len(self.groups) != self.m or min(sizes) < 1:
+            raise InvalidGroupCountError("partition must have m nonempty groups")
+        if max(sizes) - min(sizes) > 1:
+            raise InvalidGroupCountError("group sizes must differ by at most 1")
+        merged = np.concatenate(self.groups)
+        if len(np.unique(merged)) != len(merged):
+            raise InvalidGroupCountError("groups must be disjoint")
+
+
+@dataclass(frozen=True)
+class SelectionConfig:
+    """Selection knobs (selection.py:105-126). ``workers`` is accepted and
+    ignored: the device path has one result for any worker count."""
+
+    radius: float
+    tol: float
+    max_supports: int
+    m: int = 1
+    seed: int = 0
+    workers: int = 1
+
+    def __post_init__(self):
+        if self.radius <= 0:
+            raise ValueError(f"radius must be positive, got {self.radius}")
+        if self.tol <= 0:
+            raise ValueError(f"tol must be positive, got {self.tol}")
+        if self.max_supports < 3:
+            raise ValueError(f"max_supports must be >= 3, got {self.max_supports}")
+        if self.m < 1:
+            raise InvalidGroupCountError(f"m must be >= 1, got {self.m}")
+        if self.workers < 1:
+            raise ValueError(f"workers must be >= 1, got {self.workers}")
+
+
+@dataclass(frozen=True)
+class IterationRecord:
+    iteration: int
+    group: int
+    node: int
+    local_max_error: float
+    kernel_evals: int
+    cum_kernel_evals: int
+    t1_s: float
+    t2_s: float
+
+
+@dataclass(eq=False)
+class SelectionHistory:
+    records: list = field(default_factory=list)
+    seed: int = 0
+    m: int = 1
+    final_sweep: IterationRecord | None = None
+    t3_s: float | None = None
+
+
+@dataclass(eq=False)
+class SelectionResult:
+    support: SupportSet
+    history: SelectionHistory
+    converged: bool
+
+
+@dataclass
+class KernelEvalCounter:
+    count: int = 0
+
+    def add(self, n):
+        self.count += int(n)
+
+
+# ------------------------------------------------------------ host-side logic
+def _partition_positions(nb, m, seed):
+    """PCG64 permutation dealt round-robin (selection.py:183-184); returns the
+    permutation, the groups' positions concatenated and the m+1 offsets."""
+    perm = np.random.default_rng(seed).permutation(nb)
+    sizes = np.array([len(range(j, nb, m)) for j in range(m)], dtype=np.int64)
+    off = np.zeros(m + 1, dtype=np.int64)
+    np.cumsum(sizes, out=off[1:])
+    flat = np.empty(nb, dtype=np.int64)
+    for j in range(m):
+        flat[off[j] : off[j + 1]] = perm[j::m]
+    return perm, flat, off
+
+
+def partition_boundary(boundary, m, seed):
+    """Seeded balanced partition of the boundary ids (selection.py:177-185)."""
+    nb = len(boundary)
+    if not 1 <= m <= nb:
+        raise InvalidGroupCountError(f"m must be in [1, {nb}], got {m}")
+    perm = np.random.default_rng(seed).permutation(nb)
+    groups = [boundary.indices[perm[j::m]] for j in range(m)]
+    return GroupPartition(m=m, groups=groups, seed=seed)
+
+
+def seed_supports(boundary):
+    """Initial support triple (selection.py:188-195)."""
+    return boundary.indices[_seed_positions(boundary)]
+
+
+def _seed_positions(boundary):
+    """Largest |disp| first, then two farthest-point picks; first
+    occurrence wins ties (selection.py:198-212)."""
+    if len(boundary) < 3:
+        raise TooFewBoundaryNodesError(f"need at least 3 boundary nodes, got {len(boundary)}")
+    mags = np.linalg.norm(boundary.disp, axis=1)
+    chosen = [int(np.argmax(mags))]
+    dmin = np.linalg.norm(boundary.points - boundary.points[chosen[0]], axis=1)
+    for _ in range(2):
+        nxt = int(np.argmax(dmin))
+        chosen.append(nxt)
+        dmin = np.minimum(dmin, np.linalg.norm(boundary.points - boundary.points[nxt], axis=1))
+    return chosen
+
+
+def _argmax_lowest_id(errors, ids):
+    """Row of the maximum, ties to the smallest id (selection.py:231-234)."""
+    best = np.flatnonzero(errors == errors.max())
+    return int(best[np.argmin(ids[best])])
+
+
+# ------------------------------------------------------------ device scans
+def _errors_device(positions, boundary, support_points, weights, radius, want_errors=True):
+    """Fused device error scan + (err, lowest position) arg-max."""
+    lib = N.require_cuda()
+    t = N.torch()
+    pts = _to_device(boundary.points)
+    disp = _to_device(boundary.disp)
+    pos = _to_device(np.asarray(positions, dtype=np.int64), dtype=t.int64)
+    sp = _to_device(support_points)
+    w = _to_device(weights)
+    n = len(positions)
+    err = t.empty(n, dtype=t.float64, device=_device()) if want_errors else None
+    nbytes = lib.rbf_errors_scratch_bytes(n)
+    scratch = t.empty(nbytes, dtype=t.uint8, device=_device())
+    best = (N.ctypes.c_double * 2)()
+    rc = lib.rbf_errors_argmax(N.dptr(pts), N.dptr(disp), N.dptr(pos), n, N.dptr(sp), N.dptr(w),
+                               sp.shape[0], float(radius), N.dptr(err) if err is not None else None,
+                               best, N.dptr(scratch), nbytes, N.stream_ptr())
+    N.check(rc, "rbf_errors_argmax")
+    errors = _to_host(err) if err is not None else None
+    return errors, float(best[0]), int(best[1])
+
+
+def _errors_at(positions, boundary, support_points, weights, radius, workers=1):
+    """|disp - interpolant| at boundary rows (selection.py:215-221)."""
+    positions = np.asarray(positions, dtype=np.int64)
+    if len(positions) == 0:
+        return np.zeros(0)
+    errors, _, _ = _errors_device(positions, boundary, support_points, weights, radius)
+    return errors
+
+
+def interpolation_error(index, boundary, support, radius):
+    """Residual norm at one boundary node (selection.py:224-228)."""
+    pos = boundary.position_of(index)
+    predicted = evaluate_displacement(boundary.points[pos], support, radius)
+    return float(np.linalg.norm(boundary.disp[pos] - predicted))
+
+
+def group_arg_max_error(group, boundary, support, radius, counter=None):
+    """(node id, error) of the worst node in ``group`` (selection.py:237-254),
+    one fused device scan + arg-max."""
+    group = np.asarray(group, dtype=np.intp)
+    if len(group) == 0:
+        raise EmptyGroupError("group is empty")
+    positions = np.searchsorted(boundary.indices, group)
+    _, err, pos = _errors_device(positions, boundary, support.points, support.weights, radius,
+                                 want_errors=False)
+    if counter is not None:
+        counter.add(len(group) * len(support))
+    return int(boundary.indices[pos]), err
+
+
+# --------------------------------------------------------------- the loop
+class _LoopBuffers:
+    """Device buffers of one selection run; grown on RBF_EGROW."""
+
+    def __init__(self, nb, cap, rec_cap, ctas):
+        t = N.torch()
+        dev = _device()
+        self.t = t
+        self.dev = dev
+        self.nb = nb
+        self.ctas = ctas
+        self.cap = 0
+        self.rec_cap = 0
+        self.L = self.Li = self.y = self.sup = self.sel = None
+        self.records = None
+        self.inel = t.zeros(nb, dtype=t.uint8, device=dev)
+        self.state = t.zeros(N.ctypes.sizeof(N.GcbState), dtype=t.uint8, device=dev)
+        self._grow_factor(cap, 0)
+        self._grow_records(rec_cap, 0)
+
+    def _grow_factor(self, cap, n):
+        t, dev = self.t, self.dev
+        L = t.zeros(_tri(cap), dtype=t.float64, device=dev)
+        Li = t.zeros(_tri(cap), dtype=t.float64, device=dev)
+        y = t.zeros((cap, 3), dtype=t.float64, device=dev)
+        sup = t.zeros((cap, 8), dtype=t.float64, device=dev)
+        sel = t.zeros(cap, dtype=t.int32, device=dev)
+        if n:
+            L[: _tri(n)] = self.L[: _tri(n)]
+            Li[: _tri(n)] = self.Li[: _tri(n)]
+            y[:n] = self.y[:n]
+            sup[:n] = self.sup[:n]
+            sel[:n] = self.sel[:n]
+        self.L, self.Li, self.y, self.sup, self.sel, self.cap = L, Li, y, sup, sel, cap
+        lib = N.load()
+        self.scratch_bytes = lib.rbf_gcb_scratch_bytes(self.nb, cap, self.ctas)
+        self.scratch = t.empty(self.scratch_bytes, dtype=t.uint8, device=dev)
+
+    def _grow_records(self, rec_cap, nrec):
+        t = self.t
+        rec = t.zeros((rec_cap, N.RECORD_DTYPE.itemsize), dtype=t.uint8, device=self.dev)
+        if nrec:
+            rec[:nrec] = self.records[:nrec]
+        self.records, self.rec_cap = rec, rec_cap
+
+
+def _read_state(buf):
+    raw = buf.state.cpu().numpy().tobytes()
+    return N.GcbState.from_buffer_copy(raw)
+
+
+def _initial_capacity(config, nb):
+    limit = min(config.max_supports, nb)
+    return int(max(8, min(limit, 1024)))
+
+
+def gcb_select(boundary, config):
+    """Grouped-circular greedy selection (selection.py:257-271); the loop of
+    selection.py:274-421 runs on the device."""
+    return _gcb_run(boundary, config)
+
+
+def _gcb_run(boundary, config):
+    nb = len(boundary)
+    m = config.m
+    if not 1 <= m <= nb:
+        raise InvalidGroupCountError(f"m must be in [1, {nb}], got {m}")
+    radius = float(config.radius)
+    seeds = _seed_positions(boundary)  # TooFewBoundaryNodesError for nb < 3
+    lib = N.require_cuda()
+    t = N.torch()
+    _, flat, off = _partition_positions(nb, m, config.seed)
+
+    sms = N.ctypes.c_int(0)
+    ctas = N.ctypes.c_int(0)
+    N.check(lib.rbf_device_info(t.cuda.current_device(), N.ctypes.byref(sms), N.ctypes.byref(ctas)),
+            "rbf_device_info")
+    pts = _to_device(boundary.points)
+    disp = _to_device(boundary.disp)
+    gpos = _to_device(flat.astype(np.int32), dtype=t.int32)
+    goff = _to_device(off.astype(np.int32), dtype=t.int32)
+    cap = _initial_capacity(config, nb)
+    buf = _LoopBuffers(nb, cap, 2 * cap + m + 8, ctas.value)
+
+    args = N.GcbArgs()
+    args.points, args.disp = pts.data_ptr(), disp.data_ptr()
+    args.group_pos, args.group_off = gpos.data_ptr(), goff.data_ptr()
+    args.nb, args.m = nb, m
+    for q in range(3):
+        args.seeds[q] = int(seeds[q])
+    args.max_supports = int(min(config.max_supports, 2**31 - 1))
+    args.radius = radius
+    args.tol = float(config.tol)
+    args.dup_dist = NEAR_DUPLICATE_FRACTION * config.radius
+    stream = N.stream_ptr()
+    while True:
+        args.L, args.Li, args.y = buf.L.data_ptr(), buf.Li.data_ptr(), buf.y.data_ptr()
+        args.sup, args.sel, args.inel = buf.sup.data_ptr(), buf.sel.data_ptr(), buf.inel.data_ptr()
+        args.cap = buf.cap
+        args.records, args.rec_cap = buf.records.data_ptr(), buf.rec_cap
+        args.state = buf.state.data_ptr()
+        args.scratch, args.scratch_bytes = buf.scratch.data_ptr(), buf.scratch_bytes
+        N.check(lib.rbf_gcb_run(N.ctypes.byref(args), stream), "rbf_gcb_run")
+        st = _read_state(buf)
+        if st.status == N.STATUS_DONE:
+            break
+        if st.status == N.RBF_ENOTPD:
+            raise NotPositiveDefiniteError(
+                f"pivot^2 = {st.fail_pivot2:.3e} appending row {st.fail_row}; "
+                "support nodes may coincide or be nearly coincident"
+            )
+        if st.status == N.RBF_ESTALL:
+            raise SelectionStalledError(
+                "errors above tolerance remain but no group has an addable candidate"
+            )
+        if st.status != N.RBF_EGROW:
+            raise N.NativeUnavailableError(f"selection kernel ended with status {st.status}")
+        if st.n >= buf.cap:
+            if st.n >= 24576:
+                raise N.NativeUnavailableError("support count exceeds the device loop limit (24576)")
+            buf._grow_factor(min(2 * buf.cap, max(config.max_supports, 3), 24576), st.n)
+        if st.n_records >= buf.rec_cap:
+            buf._grow_records(2 * buf.rec_cap, st.n_records)
+
+    n = st.n
+    nrec = st.n_records
+    sel = _to_host(buf.sel[:n]).astype(np.intp)
+    weights = np.ascontiguousarray(_to_host(buf.sup[:n, 3:6]))
+    raw = _to_host(buf.records[:nrec]).tobytes()
+    recs = np.frombuffer(raw, dtype=N.RECORD_DTYPE)
+
+    sizes = np.diff(off)
+    history = SelectionHistory(seed=config.seed, m=m)
+    cum = 0
+    idx = boundary.indices
+    body = recs[:-1]
+    for i, r in enumerate(body):
+        evals = int(sizes[r["group"]]) * int(r["n_before"])
+        cum += evals
+        history.records.append(
+            IterationRecord(
+                iteration=3 + i,
+                group=int(r["group"]),
+                node=int(idx[r["node_pos"]]),
+                local_max_error=float(r["local_max"]),
+                kernel_evals=evals,
+                cum_kernel_evals=cum,
+                t1_s=float(r["t1_s"]),
+                t2_s=float(r["t2_s"]),
+            )
+        )
+    fin = recs[-1]
+    sweep_evals = nb * n
+    cum += sweep_evals
+    history.final_sweep = IterationRecord(
+        iteration=st.k + 1,
+        group=-1,
+        node=int(idx[fin["node_pos"]]),
+        local_max_error=float(fin["local_max"]),
+        kernel_evals=sweep_evals,
+        cum_kernel_evals=cum,
+        t1_s=float(fin["t1_s"]),
+        t2_s=float(fin["t2_s"]),
+    )
+    support = SupportSet(nodes=idx[sel], points=boundary.points[sel], weights=weights)
+    return SelectionResult(
+        support=support, history=history, converged=float(fin["local_max"]) <= config.tol
+    )
+
+
+def greedy_select(boundary, config):
+    """Traditional greedy: gcb with m = 1 (selection.py:424-428)."""
+    return gcb_select(boundary, replace(config, m=1))
+
+
+def random_select(boundary, n, seed, radius):
+    """n seeded uniform ids with solved weights (selection.py:431-442)."""
+    nb = len(boundary)
+    if not 3 <= n <= nb:
+        raise InvalidCountError(f"n must be in [3, {nb}], got {n}")
+    positions = np.random.default_rng(seed).choice(nb, size=n, replace=False)
+    points = boundary.points[positions]
+    weights = solve_support_weights(points, boundary.disp[positions], radius)
+    return SupportSet(nodes=boundary.indices[positions], points=points, weights=weights)
+
+
+def error_stage_cost(history):
+    """Error-stage kernel evaluations, final sweep excluded (selection.py:445-448)."""
+    return sum(r.kernel_evals for r in history.records)

@@ -1,0 +1,145 @@
+"""Generate golden vectors by running the REFERENCE package itself.
+
+Run here (the build container, where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+Each case is written to tests/golden/<name>.npz. Inputs come either from
+small explicit arrays (stored) or from the seeded generators in
+``paper_2004_04817_b200.workloads`` (stored as parameters plus a SHA-256 of
+the generated arrays, so tests can detect generator drift). Outputs are
+what the reference returns: the support-node sequence, weights, the
+iteration records without timing columns, the final sweep, and
+displacements at a fixed sample of volume targets.
+
+Recorded environment: numpy / scipy / OpenBLAS versions go into each file.
+"""
+
+import hashlib
+import sys
+from dataclasses import replace
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+REPO = HERE.parent.parent
+sys.path.insert(0, str(REPO))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import rbfdeform as R  # noqa: E402  (the reference)
+from rbfdeform import core as RC  # noqa: E402
+from paper_2004_04817_b200 import workloads as W  # noqa: E402
+
+
+def digest(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def env():
+    import scipy
+
+    return f"numpy {np.__version__}; scipy {scipy.__version__}"
+
+
+def run_selection(points, disp, radius, tol, max_supports, m, seed):
+    b = R.BoundarySet(indices=np.arange(len(points)), points=points, disp=disp)
+    cfg = R.SelectionConfig(radius=radius, tol=tol, max_supports=max_supports, m=m, seed=seed)
+    res = R.gcb_select(b, cfg)
+    recs = res.history.records
+    f = res.history.final_sweep
+    return {
+        "seq": np.asarray(res.support.nodes, dtype=np.int64),
+        "weights": res.support.weights,
+        "rec_iter": np.array([r.iteration for r in recs], dtype=np.int64),
+        "rec_group": np.array([r.group for r in recs], dtype=np.int64),
+        "rec_node": np.array([r.node for r in recs], dtype=np.int64),
+        "rec_local_max": np.array([r.local_max_error for r in recs], dtype=float),
+        "rec_evals": np.array([r.kernel_evals for r in recs], dtype=np.int64),
+        "rec_cum": np.array([r.cum_kernel_evals for r in recs], dtype=np.int64),
+        "final": np.array([f.iteration, f.node, f.kernel_evals, f.cum_kernel_evals], dtype=np.int64),
+        "final_max": np.array(f.local_max_error),
+        "converged": np.array(res.converged),
+        "params": np.array([radius, tol, max_supports, m, seed], dtype=float),
+    }, res
+
+
+def hemisphere():
+    rng = np.random.default_rng(7)
+    u = rng.uniform(0.0, 2.0 * np.pi, 200)
+    v = rng.uniform(0.0, 1.0, 200)
+    pts = np.column_stack([np.cos(u) * np.sqrt(1 - v**2), np.sin(u) * np.sqrt(1 - v**2), v])
+    return pts, np.tile([0.1, -0.05, 0.02], (200, 1))
+
+
+def smooth(seed):
+    rng = np.random.default_rng(seed)
+    nb = int(rng.integers(50, 501))
+    pts = rng.uniform(-1.0, 1.0, size=(nb, 3))
+    coef = rng.normal(scale=0.8, size=(3, 3))
+    disp = np.stack([0.2 * np.sin(pts @ coef[i]) for i in range(3)], axis=1)
+    return pts, disp
+
+
+def save(name, **arrays):
+    np.savez_compressed(HERE / f"{name}.npz", env=np.array(env()), **arrays)
+    print("wrote", name, {k: getattr(v, "shape", None) for k, v in arrays.items()})
+
+
+def volume_sample(wl, support, radius, n=4096):
+    idx = np.linspace(0, wl.nv - 1, min(n, wl.nv)).astype(np.int64)
+    u = R.evaluate_displacements(wl.volume[idx], support, radius)
+    return idx, u
+
+
+def main():
+    # 1. explicit small inputs (stored)
+    pts, disp = hemisphere()
+    for m in (1, 4):
+        out, _ = run_selection(pts, disp, 5.0, 1e-6, 100, m, 5)
+        save(f"hemisphere_m{m}", points=pts, disp=disp, **out)
+    for seed in (0, 3, 11):
+        pts, disp = smooth(seed)
+        for m in (1, 5):
+            out, _ = run_selection(pts, disp, 3.0, 1e-4, min(len(pts), 80), m, seed)
+            save(f"smooth{seed}_m{m}", points=pts, disp=disp, **out)
+
+    # 2. evaluation and factor known answers
+    rng = np.random.default_rng(1234)
+    sp = rng.normal(size=(700, 3))
+    sw = rng.normal(size=(700, 3))
+    q = rng.normal(size=(5000, 3)) * 2.0
+    s = R.SupportSet(nodes=np.arange(700), points=sp, weights=sw)
+    save("eval_random", sup_points=sp, sup_weights=sw, targets=q,
+         u=R.evaluate_displacements(q, s, 1.5), radius=np.array(1.5))
+    a_pts = rng.normal(size=(150, 3))
+    a = R.assemble_phi(a_pts, 3.0)
+    st = R.CholeskyState()
+    for k in range(150):
+        st.append(a[k, : k + 1])
+    rhs = rng.normal(size=(150, 3))
+    save("chol150", points=a_pts, L=st.factor, rhs=rhs, x=st.solve(rhs), radius=np.array(3.0))
+
+    # 3. BASELINE configs (generator parameters + digest; outputs)
+    for idx, ms in ((0, (1, 8)),):
+        wl = W.config(idx, nv=100_000)
+        for m in ms:
+            out, res = run_selection(wl.points, wl.disp, wl.radius, wl.tol, wl.nb, m, 0)
+            vidx, u = volume_sample(wl, res.support, wl.radius)
+            save(f"cfg{idx}_m{m}", digest=np.array(digest(wl.points, wl.disp, wl.volume)),
+                 vol_idx=vidx, vol_u=u, **out)
+    wl = W.config(1, nv=2_000_000)
+    out, res = run_selection(wl.points, wl.disp, wl.radius, wl.tol, wl.nb, 32, 0)
+    vidx, u = volume_sample(wl, res.support, wl.radius)
+    save("cfg1_m32", digest=np.array(digest(wl.points, wl.disp, wl.volume)), vol_idx=vidx, vol_u=u, **out)
+    wl = W.structured_wing(n_span=60, n_section=200, nv=100_000, m=48, name="cfg2s")
+    out, res = run_selection(wl.points, wl.disp, wl.radius, wl.tol, wl.nb, 48, 0)
+    vidx, u = volume_sample(wl, res.support, wl.radius)
+    save("cfg2s_m48", digest=np.array(digest(wl.points, wl.disp, wl.volume)), vol_idx=vidx, vol_u=u, **out)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,371 @@
+"""Parity of the sm_100a path against the reference (golden vectors made by
+running the reference itself) and the CPU oracle, through the drop-in API
+(which calls the C ABI of include/rbf_b200.h).
+
+Tolerances (floating point, FP64 throughout):
+  * support-node sequences, groups, record nodes and kernel-eval counters:
+    identical;
+  * displacements / interpolated values: 1e-9 relative to max |u|
+    (north_star), observed ~1e-13;
+  * weights: norm-wise max|dW| / max|W| <= 1e-9 where kappa(Phi) <= 1e8
+    (configs 0/1, small cases). At kappa ~ 4e9 (config-2 style grid) two
+    backward-stable solves of the same system already differ by ~2e-9
+    norm-wise, so the bar there is 2e-8.
+"""
+
+import numpy as np
+import pytest
+
+import rbf_oracle as O
+from conftest import load_golden
+from paper_2004_04817_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(b).max(), 1e-300))
+
+
+# --------------------------------------------------------------- evaluation
+def test_eval_matches_reference_golden(cuda):
+    g = load_golden("eval_random")
+    s = cuda.SupportSet(np.arange(700), g["sup_points"], g["sup_weights"])
+    u = cuda.evaluate_displacements(g["targets"], s, float(g["radius"]))
+    assert u.shape == (5000, 3) and u.dtype == np.float64 and u.flags.c_contiguous
+    assert np.abs(u - g["u"]).max() < 1e-12
+
+
+def test_eval_known_answers(cuda):
+    S = cuda.SupportSet
+    far = S(np.array([0]), np.zeros((1, 3)), np.array([[5.0, 6.0, 7.0]]))
+    assert cuda.evaluate_displacement([10.0, 0, 0], far, 2.0).tolist() == [0.0, 0.0, 0.0]
+    iso = S(np.arange(2), np.array([[0.0, 0, 0], [10.0, 0, 0]]), np.array([[1.0, 2, 3], [9.0, 9, 9]]))
+    assert cuda.evaluate_displacement([0.0, 0, 0], iso, 2.0).tolist() == [1.0, 2.0, 3.0]
+    half = S(np.array([0]), np.zeros((1, 3)), np.array([[2.0, 0, 0]]))
+    d = cuda.evaluate_displacement([1.0, 0, 0], half, 2.0)
+    assert d[0] == pytest.approx(0.375, abs=1e-15) and d[1] == 0.0 and d[2] == 0.0
+
+
+def test_eval_matches_naive_sum(cuda, rng):
+    pts = rng.normal(size=(37, 3))
+    w = rng.normal(size=(37, 3))
+    q = rng.normal(size=(211, 3)) * 2.0
+    eta = np.sqrt(((q[:, None, :] - pts[None, :, :]) ** 2).sum(-1)) / 1.5
+    expected = cuda.wendland_c2(eta) @ w
+    got = cuda.evaluate_displacements(q, cuda.SupportSet(np.arange(37), pts, w), 1.5)
+    assert np.abs(got - expected).max() < 1e-12
+
+
+def test_eval_ragged_sizes_and_tails(cuda, rng):
+    # target counts around block multiples, support counts around tile multiples
+    for nt in (1, 2, 511, 512, 513, 1537):
+        for nc in (1, 3, 127, 128, 129, 300):
+            q = rng.normal(size=(nt, 3))
+            sp = rng.normal(size=(nc, 3))
+            sw = rng.normal(size=(nc, 3))
+            got = cuda.evaluate_displacements(q, cuda.SupportSet(np.arange(nc), sp, sw), 2.0)
+            ref = O.eval_sum(q, sp, sw, 2.0)
+            assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()), (nt, nc)
+
+
+def test_eval_empty_and_errors(cuda):
+    s = cuda.SupportSet(np.array([0]), np.zeros((1, 3)), np.ones((1, 3)))
+    assert cuda.deform_points(np.empty((0, 3)), s, 1.0).shape == (0, 3)
+    with pytest.raises(ValueError):
+        cuda.evaluate_displacements(np.zeros((2, 3)), s, 0.0)
+    empty = cuda.SupportSet(np.empty(0, int), np.empty((0, 3)), np.empty((0, 3)))
+    with pytest.raises(cuda.errors.EmptySupportSetError):
+        cuda.evaluate_displacement([0, 0, 0], empty, 1.0)
+
+
+def test_deform_is_points_plus_displacement(cuda, rng):
+    pts = rng.normal(size=(40, 3))
+    s = cuda.SupportSet(np.arange(40), pts, rng.normal(size=(40, 3)))
+    q = rng.normal(size=(3000, 3))
+    q_copy = q.copy()
+    u = cuda.evaluate_displacements(q, s, 2.0)
+    moved = cuda.deform_points(q, s, 2.0)
+    assert np.array_equal(moved, q + u)
+    assert np.array_equal(q, q_copy)
+    assert np.array_equal(moved, cuda.deform_points(q, s, 2.0))
+    zero = cuda.SupportSet(np.arange(40), pts, np.zeros((40, 3)))
+    assert np.array_equal(cuda.deform_points(q, zero, 2.0), q)
+
+
+def test_eval_shards_are_bitwise_identical(cuda, rng):
+    """Per-target summation order does not depend on the launch: any split
+    of the targets (the multi-GPU sharding) reproduces the full result."""
+    pts = rng.normal(size=(333, 3))
+    s = cuda.SupportSet(np.arange(333), pts, rng.normal(size=(333, 3)))
+    q = rng.normal(size=(10_007, 3))
+    full = cuda.evaluate_displacements(q, s, 2.0)
+    for parts in (2, 3, 8):
+        cuts = np.linspace(0, len(q), parts + 1).astype(int)
+        pieces = [cuda.evaluate_displacements(q[a:b], s, 2.0) for a, b in zip(cuts[:-1], cuts[1:])]
+        assert np.array_equal(np.concatenate(pieces), full)
+    assert np.array_equal(cuda.evaluate_displacements(q, s, 2.0, workers=8), full)
+
+
+def test_eval_torch_device_path(cuda, rng):
+    import torch
+
+    pts = rng.normal(size=(50, 3))
+    s = cuda.SupportSet(np.arange(50), pts, rng.normal(size=(50, 3)))
+    q = rng.normal(size=(4000, 3))
+    qt = torch.from_numpy(q).cuda()
+    ut = cuda.evaluate_displacements(qt, s, 2.0)
+    assert isinstance(ut, torch.Tensor) and ut.is_cuda
+    assert np.array_equal(ut.cpu().numpy(), cuda.evaluate_displacements(q, s, 2.0))
+
+
+# ------------------------------------------------------------- error scans
+def test_group_arg_max_matches_oracle(cuda, rng):
+    pts = rng.normal(size=(400, 3))
+    disp = rng.normal(size=(400, 3)) * 0.1
+    b = cuda.BoundarySet(np.arange(0, 800, 2), pts, disp)
+    sp = pts[:30]
+    w = rng.normal(size=(30, 3)) * 0.05
+    s = cuda.SupportSet(b.indices[:30], sp, w)
+    group = b.indices[rng.permutation(400)[:123]]
+    counter = cuda.KernelEvalCounter()
+    node, err = cuda.group_arg_max_error(group, b, s, 3.0, counter=counter)
+    pos = np.searchsorted(b.indices, group)
+    ref = O.residual_errors(pos, pts, disp, sp, w, 3.0)
+    row = O.argmax_low(ref, group)
+    assert node == group[row]
+    assert err == pytest.approx(ref[row], rel=1e-13)
+    assert counter.count == 123 * 30
+    from paper_2004_04817_b200.selection import _errors_at
+
+    assert rel(_errors_at(pos, b, sp, w, 3.0), ref) < 1e-12
+
+
+def test_group_arg_max_ties_break_low(cuda, rng):
+    b = cuda.BoundarySet(np.arange(6), rng.normal(size=(6, 3)), np.zeros((6, 3)))
+    s = cuda.SupportSet(np.array([0]), b.points[:1], np.zeros((1, 3)))
+    node, err = cuda.group_arg_max_error(np.array([4, 1, 3]), b, s, 3.0)
+    assert node == 1 and err == 0.0
+    with pytest.raises(cuda.errors.EmptyGroupError):
+        cuda.group_arg_max_error(np.array([], dtype=int), b, s, 1.0)
+
+
+# ---------------------------------------------------------------- Cholesky
+def test_cholesky_matches_reference_golden(cuda):
+    g = load_golden("chol150")
+    a = cuda.assemble_phi(g["points"], float(g["radius"]))
+    st = cuda.CholeskyState()
+    for k in range(150):
+        st.append(a[k, : k + 1])
+    assert st.order == 150
+    assert np.abs(st.factor - g["L"]).max() < 1e-10
+    assert np.abs(st.factor - np.linalg.cholesky(a)).max() < 1e-10
+    x = st.solve(g["rhs"])
+    assert rel(x, g["x"]) < 1e-9
+    assert np.abs(a @ x - g["rhs"]).max() <= 1e-10 * max(np.abs(g["rhs"]).max(), 1.0)
+
+
+def test_cholesky_known_answers(cuda):
+    st = cuda.CholeskyState().append([4.0])
+    assert st.factor.tolist() == [[2.0]]
+    st = cuda.CholeskyState()
+    for k in range(4):
+        st.append(np.eye(4)[k, : k + 1])
+    assert np.array_equal(st.factor, np.eye(4))
+    assert st.solve(np.array([1.0, 2.0, 3.0, 4.0])).tolist() == [1.0, 2.0, 3.0, 4.0]
+    st = cuda.CholeskyState()
+    a = np.array([[1.0, 0.5], [0.5, 1.0]])
+    st.append(a[0, :1]).append(a[1, :2])
+    assert st.solve(np.array([1.0, 0.0])) == pytest.approx([4.0 / 3.0, -2.0 / 3.0], rel=1e-14)
+    assert cuda.cholesky_append(cuda.CholeskyState(), [9.0]).factor[0, 0] == 3.0
+
+
+def test_cholesky_not_pd_leaves_state(cuda):
+    st = cuda.CholeskyState().append([1.0])
+    before = st.factor
+    with pytest.raises(cuda.errors.NotPositiveDefiniteError):
+        st.append([1.0, 1.0])
+    assert st.order == 1 and np.array_equal(st.factor, before)
+    with pytest.raises(cuda.errors.DimensionMismatchError):
+        cuda.CholeskyState().append([1.0, 0.0])
+    with pytest.raises(cuda.errors.DimensionMismatchError):
+        st.solve(np.ones(3))
+
+
+def test_cholesky_growth_and_random_spd(cuda, rng):
+    for n in (2, 17, 64, 150, 300):
+        a = cuda.assemble_phi(rng.normal(size=(n, 3)), 3.0)
+        st = cuda.CholeskyState()
+        for k in range(n):
+            st.append(a[k, : k + 1])
+        L = st.factor
+        assert np.abs(L @ L.T - a).max() <= 1e-10 * np.abs(a).max(), n
+        d = rng.normal(size=(n, 3))
+        w = cuda.solve_weights(st, d)
+        assert np.abs(a @ w - d).max() <= 1e-9 * max(np.abs(d).max(), 1.0), n
+        wide = rng.normal(size=(n, 7))
+        assert np.abs(a @ st.solve(wide) - wide).max() <= 1e-9 * np.abs(wide).max()
+
+
+def test_solve_support_weights_recovers(cuda, rng):
+    pts = rng.normal(size=(20, 3)) * 2.0
+    disp = rng.normal(size=(20, 3)) * 0.1
+    w = cuda.solve_support_weights(pts, disp, 5.0)
+    s = cuda.SupportSet(np.arange(20), pts, w)
+    volume = np.vstack([rng.normal(size=(30, 3)), pts])
+    moved = cuda.deform_points(volume, s, 5.0)
+    assert np.abs(moved[30:] - (pts + disp)).max() < 1e-8
+
+
+# --------------------------------------------------------------- selection
+GOLDEN_SELECTIONS = [
+    ("hemisphere_m1", 1e-9), ("hemisphere_m4", 1e-9), ("smooth0_m1", 1e-9), ("smooth0_m5", 1e-9),
+    ("smooth3_m1", 1e-9), ("smooth3_m5", 1e-9), ("smooth11_m1", 1e-9), ("smooth11_m5", 1e-9),
+    ("cfg0_m1", 1e-9), ("cfg0_m8", 1e-9), ("cfg1_m32", 1e-9), ("cfg2s_m48", 2e-8),
+]
+
+
+def golden_inputs(name, g):
+    if "points" in g:
+        return g["points"], g["disp"], None
+    if name.startswith("cfg0"):
+        wl = W.config(0, nv=100_000)
+    elif name.startswith("cfg1"):
+        wl = W.config(1, nv=2_000_000)
+    else:
+        wl = W.structured_wing(n_span=60, n_section=200, nv=100_000, m=48, name="cfg2s")
+    return wl.points, wl.disp, wl
+
+
+@pytest.mark.parametrize("name,wtol", GOLDEN_SELECTIONS)
+def test_selection_matches_reference_golden(cuda, name, wtol):
+    g = load_golden(name)
+    pts, disp, wl = golden_inputs(name, g)
+    radius, tol, cap, m, seed = g["params"]
+    b = cuda.BoundarySet(np.arange(len(pts)), pts, disp)
+    cfg = cuda.SelectionConfig(radius=radius, tol=tol, max_supports=int(cap), m=int(m), seed=int(seed))
+    res = cuda.gcb_select(b, cfg)
+    assert np.array_equal(res.support.nodes, g["seq"]), "support-node sequence differs"
+    recs = res.history.records
+    assert [r.iteration for r in recs] == g["rec_iter"].tolist()
+    assert [r.group for r in recs] == g["rec_group"].tolist()
+    assert [r.node for r in recs] == g["rec_node"].tolist()
+    assert [r.kernel_evals for r in recs] == g["rec_evals"].tolist()
+    assert [r.cum_kernel_evals for r in recs] == g["rec_cum"].tolist()
+    lm = np.array([r.local_max_error for r in recs])
+    assert np.abs(lm - g["rec_local_max"]).max() <= 1e-9 * g["rec_local_max"].max()
+    f = res.history.final_sweep
+    assert [f.iteration, f.node, f.kernel_evals, f.cum_kernel_evals] == g["final"].tolist()
+    assert f.group == -1
+    assert f.local_max_error == pytest.approx(float(g["final_max"]), rel=1e-7, abs=1e-16)
+    assert res.converged == bool(g["converged"])
+    assert rel(res.support.weights, g["weights"]) <= wtol
+    assert np.array_equal(res.support.points, pts[g["seq"]])
+    if wl is not None:
+        u = cuda.evaluate_displacements(wl.volume[g["vol_idx"]], res.support, radius)
+        assert rel(u, g["vol_u"]) <= 1e-9
+
+
+def test_selection_determinism_and_greedy_alias(cuda):
+    g = load_golden("smooth3_m5")
+    b = cuda.BoundarySet(np.arange(len(g["points"])), g["points"], g["disp"])
+    cfg = cuda.SelectionConfig(radius=3.0, tol=1e-4, max_supports=60, m=5, seed=3)
+    a = cuda.gcb_select(b, cfg)
+    c = cuda.gcb_select(b, cfg)
+    assert np.array_equal(a.support.nodes, c.support.nodes)
+    assert np.array_equal(a.support.weights, c.support.weights)
+    from dataclasses import replace
+
+    g1 = cuda.greedy_select(b, replace(cfg, m=17))
+    m1 = cuda.gcb_select(b, replace(cfg, m=1))
+    assert np.array_equal(g1.support.nodes, m1.support.nodes)
+
+
+def test_selection_growth_path(cuda, monkeypatch):
+    """Force tiny device capacities so the loop pauses and resumes (RBF_EGROW)."""
+    from paper_2004_04817_b200 import selection as S
+
+    g = load_golden("cfg0_m8")
+    wl = W.config(0, nv=10)
+    monkeypatch.setattr(S, "_initial_capacity", lambda config, nb: 8)
+    b = cuda.BoundarySet(np.arange(wl.nb), wl.points, wl.disp)
+    res = cuda.gcb_select(b, cuda.SelectionConfig(radius=2.0, tol=wl.tol, max_supports=wl.nb, m=8))
+    assert np.array_equal(res.support.nodes, g["seq"])
+    assert [r.node for r in res.history.records] == g["rec_node"].tolist()
+    assert rel(res.support.weights, g["weights"]) <= 1e-9
+
+
+def test_selection_edge_cases(cuda, rng):
+    E = cuda.errors
+    # huge tolerance: the seeds only, converged
+    g = load_golden("hemisphere_m4")
+    b = cuda.BoundarySet(np.arange(200), g["points"], g["disp"])
+    res = cuda.gcb_select(b, cuda.SelectionConfig(radius=5.0, tol=1e9, max_supports=200, m=4))
+    assert len(res.support) == 3 and res.converged
+    assert np.array_equal(res.support.nodes, cuda.seed_supports(b))
+    # zero field: weights exactly zero
+    z = cuda.BoundarySet(np.arange(30), rng.normal(size=(30, 3)), np.zeros((30, 3)))
+    res = cuda.gcb_select(z, cuda.SelectionConfig(radius=5.0, tol=1e-6, max_supports=30, m=3))
+    assert len(res.support) == 3 and (res.support.weights == 0.0).all()
+    # m > nb
+    with pytest.raises(E.InvalidGroupCountError):
+        cuda.gcb_select(b, cuda.SelectionConfig(radius=5.0, tol=1e-6, max_supports=50, m=201))
+    # fewer than three nodes
+    with pytest.raises(E.TooFewBoundaryNodesError):
+        two = cuda.BoundarySet(np.arange(2), np.eye(3)[:2], np.zeros((2, 3)))
+        cuda.gcb_select(two, cuda.SelectionConfig(radius=1.0, tol=1e-6, max_supports=3, m=1))
+    # coincident seeds: NotPD propagates from the seed appends
+    same = cuda.BoundarySet(np.arange(4), np.zeros((4, 3)), np.ones((4, 3)))
+    with pytest.raises(E.NotPositiveDefiniteError):
+        cuda.gcb_select(same, cuda.SelectionConfig(radius=2.0, tol=1e-6, max_supports=4, m=1))
+    # cap
+    res = cuda.gcb_select(b, cuda.SelectionConfig(radius=20.0, tol=1e-12, max_supports=10, m=4))
+    assert len(res.support) == 10
+
+
+def test_selection_stall_on_contradictory_duplicates(cuda):
+    # two coincident nodes with opposite displacements (the construction of
+    # reference tests/test_selection.py:262-272)
+    pts = np.array([[0.0, 0, 0], [1.0, 0, 0], [0.0, 1, 0], [0.0, 0, 0]])
+    disp = np.zeros((4, 3))
+    disp[0] = [1.0, 0, 0]
+    disp[3] = [-1.0, 0, 0]
+    with pytest.raises(RuntimeError):
+        O.select(pts, disp, 3.0, 1e-9, 4, 1, 0)
+    b = cuda.BoundarySet(np.arange(4), pts, disp)
+    with pytest.raises(cuda.errors.SelectionStalledError):
+        cuda.gcb_select(b, cuda.SelectionConfig(radius=3.0, tol=1e-9, max_supports=4, m=1))
+
+
+def test_selection_against_oracle_fresh_inputs(cuda):
+    """Live oracle comparison on inputs not in the goldens (incl. non-trivial
+    boundary ids, which the kernel maps through positions)."""
+    for seed in (101, 202):
+        rng = np.random.default_rng(seed)
+        nb = 700
+        pts = rng.uniform(-1, 1, (nb, 3))
+        disp = 0.1 * np.sin(pts @ rng.normal(size=(3, 3)))
+        ids = np.cumsum(rng.integers(1, 5, nb))
+        for m in (1, 7):
+            ref = O.select(pts, disp, 2.5, 1e-5, nb, m, seed, ids=ids)
+            b = cuda.BoundarySet(ids, pts, disp)
+            res = cuda.gcb_select(b, cuda.SelectionConfig(radius=2.5, tol=1e-5, max_supports=nb, m=m, seed=seed))
+            assert np.array_equal(res.support.nodes, ids[ref["seq"]])
+            assert rel(res.support.weights, ref["weights"]) <= 1e-9
+            assert [r.node for r in res.history.records] == [int(ids[r[2]]) for r in ref["records"]]
+
+
+def test_estimator_drop_in(cuda, rng):
+    from sklearn.base import clone
+
+    g = load_golden("cfg0_m8")
+    wl = W.config(0, nv=5000)
+    est = cuda.RBFMeshDeformer(radius=2.0, tol=wl.tol, algorithm="gcb", m=8)
+    assert est.fit(wl.points, wl.disp) is est
+    assert np.array_equal(est.support_.nodes, g["seq"])
+    assert est.converged_ and est.n_supports_ == len(g["seq"])
+    moved = est.transform(wl.volume)
+    assert np.array_equal(moved, wl.volume + est.predict(wl.volume))
+    assert clone(est).get_params() == est.get_params()
+    with pytest.raises(ValueError):
+        cuda.RBFMeshDeformer(algorithm="nope").fit(wl.points, wl.disp)
