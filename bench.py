@@ -1,0 +1,441 @@
+#!/usr/bin/env python
+"""Benchmark: one GCB-greedy selection + volume deformation per step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+A step is the reference's hot path on one batch of synthetic input
+(BASELINE.json configs[C], default C = 1: Nb = 20,000 wing nodes,
+Nv = 2,000,000 volume nodes, GCB m = 32, R = 2, tol = 1e-4 max|d|, FP64):
+the full selection loop including the final sweep (device resident, rank 0)
+followed by deform_points over all Nv volume nodes (sharded over ranks).
+
+Metric: RBF pair-evaluations per second, whole job, with
+pairs = sum_i card(G_i) * Nc(i) + Nb * Nc   (selection, = cum_kernel_evals)
+      + Nv * Nc                              (volume).
+`value` times device-resident inputs with CUDA events; `e2e` times the same
+step through the public API with host (pinned) buffers, host<->device copies
+inside the timed region. L2 (126 MB) is flushed between timed steps by
+writing a 256 MiB buffer. Rank 0 prints ONE JSON line on stdout.
+
+--impl reference times the reference algorithm on the host CPU (the oracle
+port in oracle/, all host cores) on a bounded sample of the same workload.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+FLOP_PER_PAIR = 22  # 3 sub, 5 r^2, 1 sqrt, 1 div, 1 sub, 2 mul, 2 (4eta+1), 1 mul, 6 acc
+METRIC = "RBF pair-evals/s (GCB error + volume deform)"
+UNIT = "pair-evals/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=100_000, help="volume targets in the CPU sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(cfg):
+    from paper_2004_04817_b200 import workloads as W
+
+    return W.config(cfg)
+
+
+def config_desc(wl, world, extra=None):
+    d = {
+        "workload": f"BASELINE configs[{wl.name[-1]}]: {wl.name} wing, Nb={wl.nb}, Nv={wl.nv}, "
+                    f"GCB m={wl.m}, R={wl.radius}, tol=1e-4*max|d|, seed={wl.seed}",
+        "nb": wl.nb,
+        "nv": wl.nv,
+        "m": wl.m,
+        "radius": wl.radius,
+        "tol": wl.tol,
+        "parallelism": f"selection on rank 0, volume sharded over {world} GPU(s)",
+        "l2": "flushed between timed steps (256 MiB write)",
+    }
+    if extra:
+        d.update(extra)
+    return d
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def _target(self):
+        import torch
+
+        try:
+            uuid = str(torch.cuda.get_device_properties(self.device).uuid)
+            return uuid if uuid.startswith("GPU-") else "GPU-" + uuid
+        except Exception:
+            return str(self.device)
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "20", "-i", self._target()],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        self.lines += [ln for ln in out.splitlines() if ln.strip()]
+        self.proc = None
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        loaded = sorted(sm)[len(sm) // 2:]  # upper half = under load
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ peaks
+def measure_fp64_peak():
+    """FP64 peak on this GPU: best of our DFMA probe and cuBLAS DGEMM."""
+    import ctypes
+
+    import torch
+
+    from paper_2004_04817_b200 import _native as N
+
+    lib = N.require_cuda()
+    dev = torch.cuda.current_device()
+    scratch = torch.empty(lib.rbf_fp64_probe_scratch_bytes(dev), dtype=torch.uint8, device="cuda")
+    flops = ctypes.c_double(0)
+    best_probe = 0.0
+    for iters in (2000, 20000, 20000, 20000):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        N.check(lib.rbf_fp64_probe(iters, N.dptr(scratch), ctypes.byref(flops), N.stream_ptr()), "probe")
+        e1.record()
+        torch.cuda.synchronize()
+        best_probe = max(best_probe, flops.value / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    b = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    best_gemm = 0.0
+    for _ in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best_gemm = max(best_gemm, 2 * 8192**3 / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    del a, b
+    return {"fp64_dfma_probe_tflops": round(best_probe, 3), "fp64_dgemm_tflops": round(best_gemm, 3),
+            "peak_tflops": round(max(best_probe, best_gemm), 3),
+            "nominal_tflops": 37.0,
+            "source": "measured in this run: max(DFMA probe, cuBLAS DGEMM 8192^3); "
+                      "MEASURED_PEAKS.json has no FP64 entry"}
+
+
+def load_traffic():
+    p = REPO / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            return {}
+    return {}
+
+
+# ---------------------------------------------------------- CPU baseline
+def cpu_oracle_step(wl, threads, sample):
+    """One bounded CPU step of the reference algorithm (oracle port):
+    the full selection loop + a strided sample of the volume evaluation."""
+    sys.path.insert(0, str(REPO / "oracle"))
+    import rbf_oracle as O
+
+    t0 = time.perf_counter()
+    out = O.select(wl.points, wl.disp, wl.radius, wl.tol, wl.nb, wl.m, wl.seed, threads=threads)
+    t1 = time.perf_counter()
+    idx = np.linspace(0, wl.nv - 1, min(sample, wl.nv)).astype(np.int64)
+    O.eval_sum(wl.volume[idx], wl.points[out["seq"]], out["weights"], wl.radius, threads=threads)
+    t2 = time.perf_counter()
+    nc = len(out["seq"])
+    sel_pairs = sum(r[4] for r in out["records"]) + out["final"][3]
+    pairs = sel_pairs + len(idx) * nc
+    return {"pairs": pairs, "seconds": t2 - t0, "select_s": t1 - t0, "volume_s": t2 - t1,
+            "nc": nc, "sample": len(idx)}
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    wl = workload(args.config)
+    threads = host_threads()
+    for _ in range(max(args.warmup, 0)):
+        cpu_oracle_step(wl, threads, args.cpu_sample)
+    steps = [cpu_oracle_step(wl, threads, args.cpu_sample) for _ in range(args.steps)]
+    pairs = sum(s["pairs"] for s in steps)
+    secs = sum(s["seconds"] for s in steps)
+    value = pairs / secs
+    sample = (f"full selection loop (Nb={wl.nb}, m={wl.m}) + {steps[0]['sample']} of {wl.nv} "
+              f"volume targets per step, oracle port of the reference (numpy/scipy/OpenBLAS)")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": secs / len(steps) * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": config_desc(wl, 1, {"parallelism": f"CPU, {threads} threads"}),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "breakdown": {"select_s": statistics.mean(s["select_s"] for s in steps),
+                      "volume_sample_s": statistics.mean(s["volume_s"] for s in steps),
+                      "nc": steps[0]["nc"]},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------- GPU arm
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2004_04817_b200 as P
+    from paper_2004_04817_b200 import _native as N
+    from paper_2004_04817_b200 import multi
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    N.require_cuda()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    wl = workload(args.config)
+    peak = measure_fp64_peak()
+    boundary = P.BoundarySet(np.arange(wl.nb), wl.points, wl.disp)
+    cfg = P.SelectionConfig(radius=wl.radius, tol=wl.tol, max_supports=wl.nb, m=wl.m, seed=wl.seed)
+    lo, hi = multi.shard_range(wl.nv, rank, world)
+    nv_local = hi - lo
+    vol_d = torch.from_numpy(np.ascontiguousarray(wl.volume[lo:hi])).cuda()
+    out_d = torch.empty_like(vol_d)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def select_and_share():
+        if rank == 0:
+            res = P.gcb_select(boundary, cfg)
+            sp = torch.from_numpy(res.support.points).cuda()
+            sw = torch.from_numpy(res.support.weights).cuda()
+        else:
+            res, sp, sw = None, None, torch.empty((0, 3), dtype=torch.float64, device="cuda")
+        if world > 1:
+            sp, sw = multi.broadcast_support(sp, sw)
+        return res, sp, sw
+
+    def device_step():
+        res, sp, sw = select_and_share()
+        P.eval_device(vol_d, sp, sw, wl.radius, deform=True, out=out_d)
+        return res, sp.shape[0]
+
+    for _ in range(args.warmup):
+        device_step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    times, logs, nc, a_sel = [], [], None, None
+    for _ in range(args.steps):
+        flush.zero_()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with N.launch_log(timing=True) as log:
+            e0.record()
+            res, nc = device_step()
+            e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        times.append(e0.elapsed_time(e1) * 1e-3)
+        logs.append(log)
+        if res is not None:
+            a_sel = res.history.final_sweep.cum_kernel_evals
+    # e2e through the public API: host (pinned) buffers in and out
+    vol_host_t = torch.from_numpy(np.ascontiguousarray(wl.volume[lo:hi])).pin_memory()
+    vol_host = vol_host_t.numpy()
+    e2e_times = []
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if rank == 0:
+            res2 = P.gcb_select(P.BoundarySet(np.arange(wl.nb), wl.points, wl.disp), cfg)
+            sup = res2.support
+        if world > 1:
+            if rank == 0:
+                sp2, sw2 = torch.from_numpy(sup.points).cuda(), torch.from_numpy(sup.weights).cuda()
+            else:
+                sp2, sw2 = None, torch.empty((0, 3), dtype=torch.float64, device="cuda")
+            sp2, sw2 = multi.broadcast_support(sp2, sw2)
+            sup = P.SupportSet(np.arange(sp2.shape[0]), sp2.cpu().numpy(), sw2.cpu().numpy())
+        moved = P.deform_points(vol_host, sup, wl.radius)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        barrier()
+        if i >= args.warmup:
+            e2e_times.append(t1 - t0)
+    clocks.stop()
+    assert moved.shape == (nv_local, 3)
+
+    # ---- aggregate (max over ranks) ----
+    t_local = float(sum(times))
+    e2e_local = float(sum(e2e_times))
+    if world > 1:
+        tt = torch.tensor([t_local, e2e_local], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_total, e2e_total = tt.tolist()
+        a = torch.tensor([a_sel or 0], dtype=torch.int64, device="cuda")
+        dist.broadcast(a, src=0)
+        a_sel = int(a.item())
+    else:
+        t_total, e2e_total = t_local, e2e_local
+    pairs_per_step = a_sel + wl.nv * nc
+    value = pairs_per_step * args.steps / t_total
+    e2e_value = pairs_per_step * args.steps / e2e_total
+
+    # per-kernel device times (rank 0 view), roofline of the dominant kernel
+    sel_ms = [ms for lg in logs for ms in lg.kernel_ms("rbf_gcb_run")]
+    vol_ms = [ms for lg in logs for ms in lg.kernel_ms("rbf_eval")]
+    launches = sum(lg.count for lg in logs) / len(logs)
+    traffic = load_traffic()
+    peak_tf = peak["peak_tflops"]
+    kernels = []
+    if sel_ms:
+        t = statistics.mean(sel_ms) * 1e-3
+        ach = FLOP_PER_PAIR * a_sel / t / 1e12
+        kernels.append({"kernel": "gcb_kernel (selection loop, 1 launch)", "ms": t * 1e3,
+                        "bound": "latency (grid barriers) / fp64", "achieved": ach, "peak": peak_tf,
+                        "unit": "TFLOP/s", "frac": ach / peak_tf,
+                        "traffic": traffic.get("gcb_kernel")})
+    if vol_ms:
+        t = statistics.mean(vol_ms) * 1e-3
+        ach = FLOP_PER_PAIR * nv_local * nc / t / 1e12
+        kernels.append({"kernel": "eval_kernel<deform> (volume)", "ms": t * 1e3, "bound": "fp64",
+                        "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s", "frac": ach / peak_tf,
+                        "traffic": traffic.get("eval_kernel")})
+    dominant = max(kernels, key=lambda k: k["ms"]) if kernels else None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = host_threads()
+        s = cpu_oracle_step(wl, threads, args.cpu_sample)
+        cpu = {"value": s["pairs"] / s["seconds"], "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"full selection loop + {s['sample']} of {wl.nv} volume targets, oracle "
+                         f"port (numpy/scipy/OpenBLAS, {threads} threads), {s['seconds']:.2f} s"}
+
+    if rank == 0:
+        h2d = (wl.nb * 48 + wl.nb * 4 + (wl.m + 1) * 4 + nv_local * 24 + nc * 48)
+        d2h = (nv_local * 24 + nc * (4 + 24) + 64 + 40 * (len(res.history.records) + 1))
+        roof = None
+        if dominant:
+            roof = {"bound": "fp64", "achieved": dominant["achieved"], "peak": peak_tf,
+                    "unit": "TFLOP/s", "frac": dominant["frac"], "traffic": dominant["traffic"],
+                    "kernel": dominant["kernel"], "peak_source": peak["source"]}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_total / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, paper_2004_04817_b200/workloads.py)",
+            "config": config_desc(wl, world),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps * 1e3},
+            "roofline": roof,
+            "kernels": kernels,
+            "fp64_peak": peak,
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+            "gpu_launches": launches,
+            "breakdown": {"nc": nc, "selection_pairs": a_sel, "volume_pairs": wl.nv * nc,
+                          "iterations": len(res.history.records),
+                          "selection_ms": statistics.mean(sel_ms) if sel_ms else None,
+                          "volume_ms": statistics.mean(vol_ms) if vol_ms else None,
+                          "converged": bool(res.converged),
+                          "loop_mode": getattr(res.history, "device_mode", None),
+                          "loop_phase_us": {k: v / 1.965e3 for k, v in
+                                            getattr(res.history, "device_phase_cycles", {}).items()
+                                            if k not in ("appends", "iterations")},
+                          "loop_counts": {k: getattr(res.history, "device_phase_cycles", {}).get(k)
+                                          for k in ("appends", "iterations")}},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -117,17 +117,20 @@ RBF_API int rbf_chol_solve(const double* L, const double* Li, int64_t n,
 /* ---------------------------------------------------------------------
  * The GCB / greedy selection loop, fully device resident.
  * Replaces selection.py:274-421 `_gcb_run` (entry points gcb_select
- * selection.py:257-271 and greedy_select selection.py:424-428).
+ * selection.py:257-271 and greedy_select selection.py:424-428), including
+ * the seeds (selection.py:198-212, bit-exact norms and first-occurrence
+ * arg-max) and the final sweep.
  *
- * The host does what must stay bit-identical to numpy: the PCG64
- * partition (selection.py:177-185) and the three seeds
- * (selection.py:198-212); it passes them in. One cooperative persistent
- * kernel then runs seeding appends, every iteration (weights update,
- * group scan + arg-max, candidate walk with near-duplicate and pivot
- * rejection, factor append), the termination logic and the final sweep.
- * It returns RBF_EGROW when the factor or record buffers are full: the host
- * grows them (packed prefixes are capacity independent) and calls again
- * with the same state, which resumes the same iteration.
+ * The host does what must stay bit-identical to numpy's PCG64: the
+ * partition (selection.py:177-185); it passes the groups in. One
+ * persistent kernel then runs everything else. Two launch shapes share the
+ * code: a single 16-CTA thread-block cluster synchronised by hardware
+ * cluster barriers (small and medium problems: every phase is latency
+ * bound), or a cooperative grid of one CTA per SM with a software grid
+ * barrier (large group scans). It returns RBF_EGROW when the factor or
+ * record buffers are full: the host grows them (packed prefixes are
+ * capacity independent) and calls again with the same state, which resumes
+ * the same iteration.
  */
 typedef struct rbf_gcb_record {
   int32_t group;      /* group visited (-1 for the final sweep)             */
@@ -153,7 +156,13 @@ typedef struct rbf_gcb_state {
   double final_max;     /* final sweep */
   int32_t final_pos;
   int32_t fault;        /* watchdog flag                                   */
+  /* diagnostics: SM cycles CTA 0 spent per phase, summed over the run:
+   * [0] scan+barrier, [1] fold+row, [2] c0, [3] r, [4] c, [5] pivot+cols,
+   * [6] bookkeeping, [7] seeds, [8] final sweep, [9] appends, [10] iterations */
+  double phase_cycles[12];
 } rbf_gcb_state;
+
+enum { RBF_GCB_AUTO = 0, RBF_GCB_CLUSTER = 1, RBF_GCB_GRID = 2 };
 
 typedef struct rbf_gcb_args {
   /* boundary (device) */
@@ -162,7 +171,7 @@ typedef struct rbf_gcb_args {
   const int32_t* group_pos; /* (nb) positions, groups concatenated        */
   const int32_t* group_off; /* (m + 1) offsets into group_pos              */
   int32_t nb, m;
-  int32_t seeds[3];         /* seed positions (host computed)             */
+  int32_t mode;             /* RBF_GCB_AUTO / _CLUSTER / _GRID             */
   int32_t max_supports;
   double radius, tol;
   double dup_dist;          /* NEAR_DUPLICATE_FRACTION * radius            */
@@ -170,7 +179,7 @@ typedef struct rbf_gcb_args {
   double* L;                /* packed, cap*(cap+1)/2 */
   double* Li;               /* packed, cap*(cap+1)/2 */
   double* y;                /* (cap, 3) forward-substituted displacements */
-  double* sup;              /* (cap, 8) scaled x,y,z, weights wx,wy,wz, 2 pad */
+  double* sup;              /* (6, cap) SoA: x, y, z, wx, wy, wz           */
   int32_t* sel;             /* (cap) selected positions in order          */
   uint8_t* inel;            /* (nb) ineligible flags                       */
   int32_t cap;
@@ -183,10 +192,23 @@ typedef struct rbf_gcb_args {
   size_t scratch_bytes;
 } rbf_gcb_args;
 
+/* CTAs the selection kernel uses in `mode` for a problem of nb nodes and
+ * m groups (mode AUTO picks cluster or grid). */
+RBF_API int rbf_gcb_ctas(int32_t mode, int32_t nb, int32_t m, int32_t* ctas_host,
+                         int32_t* resolved_mode_host);
 RBF_API size_t rbf_gcb_scratch_bytes(int32_t nb, int32_t cap, int32_t ctas);
 /* Launch (asynchronous). The caller zero-initialises *state (n = 0) and
  * inel before the first call. */
 RBF_API int rbf_gcb_run(const rbf_gcb_args* args, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Diagnostics (no reference counterpart): an FP64 DFMA throughput probe
+ * used to measure the FP64 peak the roofline fractions are quoted against.
+ * `scratch` holds rbf_fp64_probe_scratch_bytes(device) bytes; `flops_host`
+ * receives the FP64 operations the launch performs (time it with events).
+ */
+RBF_API size_t rbf_fp64_probe_scratch_bytes(int device);
+RBF_API int rbf_fp64_probe(int iters, double* scratch, double* flops_host, void* stream);
 
 #ifdef __cplusplus
 }

@@ -22,6 +22,9 @@ RBF_ENCCL = 4
 RBF_EGROW = 5
 RBF_ESTALL = 6
 STATUS_DONE = 1
+GCB_AUTO = 0
+GCB_CLUSTER = 1
+GCB_GRID = 2
 
 c_dp = ctypes.c_void_p  # device pointers are passed as integers
 
@@ -60,10 +63,13 @@ class GcbState(ctypes.Structure):
         ("final_max", ctypes.c_double),
         ("final_pos", ctypes.c_int32),
         ("fault", ctypes.c_int32),
+        ("phase_cycles", ctypes.c_double * 12),
     ]
 
 
-assert ctypes.sizeof(GcbState) == 64
+assert ctypes.sizeof(GcbState) == 160
+PHASES = ["scan", "fold_row", "c0", "r", "c", "pivot_cols", "bookkeeping", "seeds", "final_sweep",
+          "appends", "iterations"]
 
 
 class GcbArgs(ctypes.Structure):
@@ -74,7 +80,7 @@ class GcbArgs(ctypes.Structure):
         ("group_off", c_dp),
         ("nb", ctypes.c_int32),
         ("m", ctypes.c_int32),
-        ("seeds", ctypes.c_int32 * 3),
+        ("mode", ctypes.c_int32),
         ("max_supports", ctypes.c_int32),
         ("radius", ctypes.c_double),
         ("tol", ctypes.c_double),
@@ -111,8 +117,13 @@ SIGNATURES = [
      [c_dp, c_dp, ctypes.c_int64, c_dp, ctypes.POINTER(ctypes.c_double), c_dp, ctypes.c_size_t, c_dp]),
     ("rbf_chol_solve", ctypes.c_int,
      [c_dp, c_dp, ctypes.c_int64, c_dp, ctypes.c_int64, c_dp, c_dp, ctypes.c_size_t, c_dp]),
+    ("rbf_gcb_ctas", ctypes.c_int,
+     [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+      ctypes.POINTER(ctypes.c_int32)]),
     ("rbf_gcb_scratch_bytes", ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
     ("rbf_gcb_run", ctypes.c_int, [ctypes.POINTER(GcbArgs), c_dp]),
+    ("rbf_fp64_probe_scratch_bytes", ctypes.c_size_t, [ctypes.c_int]),
+    ("rbf_fp64_probe", ctypes.c_int, [ctypes.c_int, c_dp, ctypes.POINTER(ctypes.c_double), c_dp]),
 ]
 
 _lib = None
@@ -195,3 +206,66 @@ def stream_ptr(stream=None):
 
 def dptr(tensor):
     return ctypes.c_void_p(tensor.data_ptr())
+
+
+# ------------------------------------------------------ launch accounting
+class LaunchLog:
+    """Counts this library's kernel launches and (optionally) brackets them
+    with CUDA events on the launching stream, for bench.py's per-kernel
+    timings and its ``gpu_launches`` figure."""
+
+    def __init__(self, timing=False):
+        self.timing = timing
+        self.count = 0
+        self.by_name = {}
+        self.spans = []  # (name, start_event, end_event)
+
+    def kernel_ms(self, name):
+        torch().cuda.synchronize()
+        return [a.elapsed_time(b) for n, a, b in self.spans if n == name]
+
+
+_log = None
+
+
+class launch_log:
+    def __init__(self, timing=False):
+        self.log = LaunchLog(timing)
+
+    def __enter__(self):
+        global _log
+        self._prev = _log
+        _log = self.log
+        return self.log
+
+    def __exit__(self, *exc):
+        global _log
+        _log = self._prev
+        return False
+
+
+class launching:
+    """``with launching("rbf_eval", kernels=1): rc = lib.rbf_eval(...)``"""
+
+    def __init__(self, name, kernels=1):
+        self.name = name
+        self.kernels = kernels
+
+    def __enter__(self):
+        log = _log
+        if log is not None:
+            log.count += self.kernels
+            log.by_name[self.name] = log.by_name.get(self.name, 0) + self.kernels
+            if log.timing:
+                t = torch()
+                self.e0 = t.cuda.Event(enable_timing=True)
+                self.e1 = t.cuda.Event(enable_timing=True)
+                self.e0.record()
+        return self
+
+    def __exit__(self, *exc):
+        log = _log
+        if log is not None and log.timing:
+            self.e1.record()
+            log.spans.append((self.name, self.e0, self.e1))
+        return False

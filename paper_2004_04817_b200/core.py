@@ -172,8 +172,9 @@ class CholeskyState:
         nbytes = lib.rbf_chol_scratch_bytes(n + 1)
         scratch = t.empty(nbytes, dtype=t.uint8, device=_device())
         piv = N.ctypes.c_double(0.0)
-        rc = lib.rbf_chol_append(N.dptr(self._L), N.dptr(self._Li), n, N.dptr(row),
-                                 N.ctypes.byref(piv), N.dptr(scratch), nbytes, N.stream_ptr())
+        with N.launching("rbf_chol_append", kernels=6 if n else 2):
+            rc = lib.rbf_chol_append(N.dptr(self._L), N.dptr(self._Li), n, N.dptr(row),
+                                     N.ctypes.byref(piv), N.dptr(scratch), nbytes, N.stream_ptr())
         if rc == N.RBF_ENOTPD:
             raise NotPositiveDefiniteError(
                 f"pivot^2 = {piv.value:.3e} appending row {n}; "
@@ -198,8 +199,9 @@ class CholeskyState:
         out = t.empty_like(b)
         nbytes = 3 * self._n * k * 8
         scratch = t.empty(nbytes, dtype=t.uint8, device=_device())
-        rc = lib.rbf_chol_solve(N.dptr(self._L), N.dptr(self._Li), self._n, N.dptr(b), k,
-                                N.dptr(out), N.dptr(scratch), nbytes, N.stream_ptr())
+        with N.launching("rbf_chol_solve", kernels=6 * ((k + 3) // 4)):
+            rc = lib.rbf_chol_solve(N.dptr(self._L), N.dptr(self._Li), self._n, N.dptr(b), k,
+                                    N.dptr(out), N.dptr(scratch), nbytes, N.stream_ptr())
         N.check(rc, "rbf_chol_solve")
         return _to_host(out).reshape(rhs.shape)
 
@@ -276,9 +278,10 @@ def eval_device(points, support_points, weights, radius, deform=False, out=None)
     n = points.shape[0]
     if out is None:
         out = t.empty((n, 3), dtype=t.float64, device=points.device)
-    rc = lib.rbf_eval(N.dptr(points), n, N.dptr(support_points), N.dptr(weights),
-                      support_points.shape[0], float(radius), 1 if deform else 0,
-                      N.dptr(out), N.stream_ptr())
+    with N.launching("rbf_eval", kernels=1 if n else 0):
+        rc = lib.rbf_eval(N.dptr(points), n, N.dptr(support_points), N.dptr(weights),
+                          support_points.shape[0], float(radius), 1 if deform else 0,
+                          N.dptr(out), N.stream_ptr())
     N.check(rc, "rbf_eval")
     return out
 

@@ -221,9 +221,10 @@ def _errors_device(positions, boundary, support_points, weights, radius, want_er
     nbytes = lib.rbf_errors_scratch_bytes(n)
     scratch = t.empty(nbytes, dtype=t.uint8, device=_device())
     best = (N.ctypes.c_double * 2)()
-    rc = lib.rbf_errors_argmax(N.dptr(pts), N.dptr(disp), N.dptr(pos), n, N.dptr(sp), N.dptr(w),
-                               sp.shape[0], float(radius), N.dptr(err) if err is not None else None,
-                               best, N.dptr(scratch), nbytes, N.stream_ptr())
+    with N.launching("rbf_errors_argmax", kernels=2):
+        rc = lib.rbf_errors_argmax(N.dptr(pts), N.dptr(disp), N.dptr(pos), n, N.dptr(sp), N.dptr(w),
+                                   sp.shape[0], float(radius), N.dptr(err) if err is not None else None,
+                                   best, N.dptr(scratch), nbytes, N.stream_ptr())
     N.check(rc, "rbf_errors_argmax")
     errors = _to_host(err) if err is not None else None
     return errors, float(best[0]), int(best[1])
@@ -281,16 +282,17 @@ class _LoopBuffers:
 
     def _grow_factor(self, cap, n):
         t, dev = self.t, self.dev
-        L = t.zeros(_tri(cap), dtype=t.float64, device=dev)
-        Li = t.zeros(_tri(cap), dtype=t.float64, device=dev)
-        y = t.zeros((cap, 3), dtype=t.float64, device=dev)
-        sup = t.zeros((cap, 8), dtype=t.float64, device=dev)
-        sel = t.zeros(cap, dtype=t.int32, device=dev)
+        # every row is written by the kernel before it is read: no zero fill
+        L = t.empty(_tri(cap), dtype=t.float64, device=dev)
+        Li = t.empty(_tri(cap), dtype=t.float64, device=dev)
+        y = t.empty((cap, 3), dtype=t.float64, device=dev)
+        sup = t.empty((6, cap), dtype=t.float64, device=dev)  # SoA: x, y, z, wx, wy, wz
+        sel = t.empty(cap, dtype=t.int32, device=dev)
         if n:
             L[: _tri(n)] = self.L[: _tri(n)]
             Li[: _tri(n)] = self.Li[: _tri(n)]
             y[:n] = self.y[:n]
-            sup[:n] = self.sup[:n]
+            sup[:, :n] = self.sup[:, :n]
             sel[:n] = self.sel[:n]
         self.L, self.Li, self.y, self.sup, self.sel, self.cap = L, Li, y, sup, sel, cap
         lib = N.load()
@@ -299,7 +301,7 @@ class _LoopBuffers:
 
     def _grow_records(self, rec_cap, nrec):
         t = self.t
-        rec = t.zeros((rec_cap, N.RECORD_DTYPE.itemsize), dtype=t.uint8, device=self.dev)
+        rec = t.empty((rec_cap, N.RECORD_DTYPE.itemsize), dtype=t.uint8, device=self.dev)
         if nrec:
             rec[:nrec] = self.records[:nrec]
         self.records, self.rec_cap = rec, rec_cap
@@ -310,8 +312,11 @@ def _read_state(buf):
     return N.GcbState.from_buffer_copy(raw)
 
 
+_DEVICE_MAX_SUPPORTS = 8192  # kRowSmemMax in csrc/rbf_gcb.cu
+
+
 def _initial_capacity(config, nb):
-    limit = min(config.max_supports, nb)
+    limit = min(config.max_supports, nb) + 1
     return int(max(8, min(limit, 1024)))
 
 
@@ -321,21 +326,23 @@ def gcb_select(boundary, config):
     return _gcb_run(boundary, config)
 
 
-def _gcb_run(boundary, config):
+def _gcb_run(boundary, config, mode=None):
     nb = len(boundary)
     m = config.m
     if not 1 <= m <= nb:
         raise InvalidGroupCountError(f"m must be in [1, {nb}], got {m}")
+    if nb < 3:
+        raise TooFewBoundaryNodesError(f"need at least 3 boundary nodes, got {nb}")
     radius = float(config.radius)
-    seeds = _seed_positions(boundary)  # TooFewBoundaryNodesError for nb < 3
     lib = N.require_cuda()
     t = N.torch()
     _, flat, off = _partition_positions(nb, m, config.seed)
 
-    sms = N.ctypes.c_int(0)
-    ctas = N.ctypes.c_int(0)
-    N.check(lib.rbf_device_info(t.cuda.current_device(), N.ctypes.byref(sms), N.ctypes.byref(ctas)),
-            "rbf_device_info")
+    ctas = N.ctypes.c_int32(0)
+    resolved = N.ctypes.c_int32(0)
+    want = N.GCB_AUTO if mode is None else mode
+    N.check(lib.rbf_gcb_ctas(want, nb, m, N.ctypes.byref(ctas), N.ctypes.byref(resolved)),
+            "rbf_gcb_ctas")
     pts = _to_device(boundary.points)
     disp = _to_device(boundary.disp)
     gpos = _to_device(flat.astype(np.int32), dtype=t.int32)
@@ -347,13 +354,13 @@ def _gcb_run(boundary, config):
     args.points, args.disp = pts.data_ptr(), disp.data_ptr()
     args.group_pos, args.group_off = gpos.data_ptr(), goff.data_ptr()
     args.nb, args.m = nb, m
-    for q in range(3):
-        args.seeds[q] = int(seeds[q])
+    args.mode = resolved.value
     args.max_supports = int(min(config.max_supports, 2**31 - 1))
     args.radius = radius
     args.tol = float(config.tol)
     args.dup_dist = NEAR_DUPLICATE_FRACTION * config.radius
     stream = N.stream_ptr()
+    limit = min(config.max_supports, nb) + 1
     while True:
         args.L, args.Li, args.y = buf.L.data_ptr(), buf.Li.data_ptr(), buf.y.data_ptr()
         args.sup, args.sel, args.inel = buf.sup.data_ptr(), buf.sel.data_ptr(), buf.inel.data_ptr()
@@ -361,7 +368,9 @@ def _gcb_run(boundary, config):
         args.records, args.rec_cap = buf.records.data_ptr(), buf.rec_cap
         args.state = buf.state.data_ptr()
         args.scratch, args.scratch_bytes = buf.scratch.data_ptr(), buf.scratch_bytes
-        N.check(lib.rbf_gcb_run(N.ctypes.byref(args), stream), "rbf_gcb_run")
+        with N.launching("rbf_gcb_run", kernels=1):
+            rc = lib.rbf_gcb_run(N.ctypes.byref(args), stream)
+        N.check(rc, "rbf_gcb_run")
         st = _read_state(buf)
         if st.status == N.STATUS_DONE:
             break
@@ -377,16 +386,17 @@ def _gcb_run(boundary, config):
         if st.status != N.RBF_EGROW:
             raise N.NativeUnavailableError(f"selection kernel ended with status {st.status}")
         if st.n >= buf.cap:
-            if st.n >= 24576:
-                raise N.NativeUnavailableError("support count exceeds the device loop limit (24576)")
-            buf._grow_factor(min(2 * buf.cap, max(config.max_supports, 3), 24576), st.n)
+            if st.n >= _DEVICE_MAX_SUPPORTS:
+                raise N.NativeUnavailableError(
+                    f"support count exceeds the device loop limit ({_DEVICE_MAX_SUPPORTS})")
+            buf._grow_factor(max(min(2 * buf.cap, limit, _DEVICE_MAX_SUPPORTS), st.n + 1), st.n)
         if st.n_records >= buf.rec_cap:
             buf._grow_records(2 * buf.rec_cap, st.n_records)
 
     n = st.n
     nrec = st.n_records
     sel = _to_host(buf.sel[:n]).astype(np.intp)
-    weights = np.ascontiguousarray(_to_host(buf.sup[:n, 3:6]))
+    weights = np.ascontiguousarray(_to_host(buf.sup[3:6, :n]).T)
     raw = _to_host(buf.records[:nrec]).tobytes()
     recs = np.frombuffer(raw, dtype=N.RECORD_DTYPE)
 
@@ -423,6 +433,9 @@ def _gcb_run(boundary, config):
         t1_s=float(fin["t1_s"]),
         t2_s=float(fin["t2_s"]),
     )
+    # diagnostics: SM cycles of CTA 0 per phase of the device loop
+    history.device_phase_cycles = dict(zip(N.PHASES, list(st.phase_cycles)))
+    history.device_mode = "cluster" if args.mode == N.GCB_CLUSTER else "grid"
     support = SupportSet(nodes=idx[sel], points=boundary.points[sel], weights=weights)
     return SelectionResult(
         support=support, history=history, converged=float(fin["local_max"]) <= config.tol

@@ -369,3 +369,23 @@ def test_estimator_drop_in(cuda, rng):
     assert clone(est).get_params() == est.get_params()
     with pytest.raises(ValueError):
         cuda.RBFMeshDeformer(algorithm="nope").fit(wl.points, wl.disp)
+
+
+@pytest.mark.parametrize("name", ["cfg0_m8", "cfg0_m1", "smooth0_m5", "hemisphere_m4"])
+def test_selection_cluster_and_grid_modes(cuda, name):
+    """Both launch shapes of the loop kernel (one 16-CTA cluster with
+    hardware barriers; a cooperative grid of one CTA per SM) reproduce the
+    reference sequence."""
+    from paper_2004_04817_b200 import _native as N
+    from paper_2004_04817_b200.selection import _gcb_run
+
+    g = load_golden(name)
+    pts, disp, _ = golden_inputs(name, g)
+    radius, tol, cap, m, seed = g["params"]
+    b = cuda.BoundarySet(np.arange(len(pts)), pts, disp)
+    cfg = cuda.SelectionConfig(radius=radius, tol=tol, max_supports=int(cap), m=int(m), seed=int(seed))
+    for mode in (N.GCB_CLUSTER, N.GCB_GRID):
+        res = _gcb_run(b, cfg, mode=mode)
+        assert np.array_equal(res.support.nodes, g["seq"]), mode
+        assert [r.node for r in res.history.records] == g["rec_node"].tolist()
+        assert rel(res.support.weights, g["weights"]) <= 1e-9

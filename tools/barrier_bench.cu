@@ -1,0 +1,72 @@
+// Microbenchmark: grid-wide software barrier (as in rbf_common.cuh) vs.
+// hardware cluster barrier, on the B200. Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o barrier_bench barrier_bench.cu
+#include <cstdio>
+#include <cooperative_groups.h>
+#include "../paper_2004_04817_b200/csrc/rbf_common.cuh"
+namespace cg = cooperative_groups;
+
+__global__ void grid_bar_kernel(rbf::GridBarrier* bar, int* fault, int iters, unsigned long long* out) {
+  unsigned long long t0 = rbf::globaltimer_ns();
+  for (int i = 0; i < iters; ++i) rbf::grid_sync(bar, gridDim.x, fault);
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = rbf::globaltimer_ns() - t0;
+}
+
+__global__ void cg_grid_kernel(int iters, unsigned long long* out) {
+  cg::grid_group g = cg::this_grid();
+  unsigned long long t0 = rbf::globaltimer_ns();
+  for (int i = 0; i < iters; ++i) g.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[1] = rbf::globaltimer_ns() - t0;
+}
+
+__global__ void cluster_bar_kernel(int iters, unsigned long long* out, int slot) {
+  cg::cluster_group c = cg::this_cluster();
+  unsigned long long t0 = rbf::globaltimer_ns();
+  for (int i = 0; i < iters; ++i) c.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[slot] = rbf::globaltimer_ns() - t0;
+}
+
+// L2 latency: dependent pointer chase over a small array (stays in L2)
+__global__ void chase_kernel(const int* next, int steps, unsigned long long* out, int* sink) {
+  int p = 0;
+  unsigned long long t0 = rbf::globaltimer_ns();
+  for (int i = 0; i < steps; ++i) p = __ldcg(next + p);
+  out[5] = rbf::globaltimer_ns() - t0;
+  sink[0] = p;
+}
+
+int main() {
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  rbf::GridBarrier* bar; int* fault; unsigned long long* out;
+  cudaMalloc(&bar, 64); cudaMemset(bar, 0, 64); cudaMalloc(&fault, 4); cudaMalloc(&out, 64);
+  cudaMemset(out, 0, 64);
+  int iters = 20000;
+  void* a1[] = {&bar, &fault, &iters, &out};
+  cudaLaunchCooperativeKernel((void*)grid_bar_kernel, sms, 512, a1, 0, 0);
+  void* a2[] = {&iters, &out};
+  cudaLaunchCooperativeKernel((void*)cg_grid_kernel, sms, 512, a2, 0, 0);
+  for (int cs : {8, 16}) {
+    cudaFuncSetAttribute(cluster_bar_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs); cfg.blockDim = dim3(512);
+    cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    int slot = cs == 8 ? 2 : 3;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, cluster_bar_kernel, iters, out, slot);
+    if (e != cudaSuccess) printf("cluster %d launch: %s\n", cs, cudaGetErrorString(e));
+  }
+  int n = 1 << 16; int* next; cudaMalloc(&next, n * 4);
+  int* h = new int[n]; for (int i = 0; i < n; ++i) h[i] = (i * 7919 + 13) % n;
+  cudaMemcpy(next, h, n * 4, cudaMemcpyHostToDevice);
+  int* sink; cudaMalloc(&sink, 4);
+  chase_kernel<<<1, 1>>>(next, 20000, out, sink);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long r[8]; cudaMemcpy(r, out, 64, cudaMemcpyDeviceToHost);
+  printf("status %s\n", cudaGetErrorString(e));
+  printf("grid barrier (ours, %d CTAs x 512): %.3f us/barrier\n", sms, r[0] / 1e3 / iters);
+  printf("grid barrier (cg::grid.sync):        %.3f us/barrier\n", r[1] / 1e3 / iters);
+  printf("cluster barrier (8 CTAs):            %.3f us/barrier\n", r[2] / 1e3 / iters);
+  printf("cluster barrier (16 CTAs):           %.3f us/barrier\n", r[3] / 1e3 / iters);
+  printf("L2 dependent load latency:           %.1f ns\n", r[5] / 20000.0);
+  return 0;
+}
