@@ -156,13 +156,23 @@ typedef struct rbf_gcb_state {
   double final_max;     /* final sweep */
   int32_t final_pos;
   int32_t fault;        /* watchdog flag                                   */
+  int32_t want_mode;    /* on RBF_EGROW: mode the kernel asks to resume in  */
+  int32_t pad_;
   /* diagnostics: SM cycles CTA 0 spent per phase, summed over the run:
    * [0] scan+barrier, [1] fold+row, [2] c0, [3] r, [4] c, [5] pivot+cols,
    * [6] bookkeeping, [7] seeds, [8] final sweep, [9] appends, [10] iterations */
   double phase_cycles[12];
 } rbf_gcb_state;
 
-enum { RBF_GCB_AUTO = 0, RBF_GCB_CLUSTER = 1, RBF_GCB_GRID = 2 };
+/* Launch shapes of the selection kernel:
+ *  SMEM    one 16-CTA cluster; supports, weights and the Cholesky work
+ *          vectors replicated in every CTA's shared memory (written through
+ *          distributed shared memory), the factor rows in L2 (n < 1024);
+ *  CLUSTER one 16-CTA cluster, all state in global memory (L2);
+ *  GRID    one CTA per SM (cooperative), all state in global memory.
+ * AUTO picks SMEM for group sizes up to 2048 (the kernel asks to resume in
+ * CLUSTER once n reaches 1024) and GRID above. */
+enum { RBF_GCB_AUTO = 0, RBF_GCB_CLUSTER = 1, RBF_GCB_GRID = 2, RBF_GCB_SMEM = 3 };
 
 typedef struct rbf_gcb_args {
   /* boundary (device) */

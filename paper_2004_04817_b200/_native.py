@@ -25,6 +25,7 @@ STATUS_DONE = 1
 GCB_AUTO = 0
 GCB_CLUSTER = 1
 GCB_GRID = 2
+GCB_SMEM = 3
 
 c_dp = ctypes.c_void_p  # device pointers are passed as integers
 
@@ -63,11 +64,13 @@ class GcbState(ctypes.Structure):
         ("final_max", ctypes.c_double),
         ("final_pos", ctypes.c_int32),
         ("fault", ctypes.c_int32),
+        ("want_mode", ctypes.c_int32),
+        ("pad_", ctypes.c_int32),
         ("phase_cycles", ctypes.c_double * 12),
     ]
 
 
-assert ctypes.sizeof(GcbState) == 160
+assert ctypes.sizeof(GcbState) == 168
 PHASES = ["scan", "fold_row", "c0", "r", "c", "pivot_cols", "bookkeeping", "seeds", "final_sweep",
           "appends", "iterations"]
 

@@ -8,8 +8,8 @@
 // agree bit for bit and the only synchronisation is a team barrier between
 // data-parallel phases:
 //
-//   scan   supports staged into shared memory (SoA), group errors, per-CTA
-//          (err, lowest position) partials for all and for eligible nodes   | B1
+//   scan   group errors, per-CTA (err, lowest position) partials for all and
+//          for eligible nodes                                                | B1
 //   append row phi(|p - s_j|/R) (reference arithmetic, every CTA), then
 //          c0 = Li row                                                        | B2
 //          r  = row - L c0                                                    | B3
@@ -18,11 +18,16 @@
 //          u = Li^T c, v = Li^T y  ->  Li[n] = -u/l, weights v + Li[n] y_n,
 //          L[n] = [c, l]                                                      | B5
 //
-// Team = one 16-CTA thread-block cluster (hardware barrier.cluster, ~0.3 us)
-// for small and medium problems, or a cooperative grid of one CTA per SM
-// with a single-word software barrier (~1.2 us) when group scans are large.
-// Every loop in a phase issues its global loads back to back (unrolled), so
-// a phase costs about one L2 round trip (~160 ns on B200) plus its math.
+// Two storage paths behind one driver (gcb_driver):
+//  * SmemPath: one 16-CTA thread-block cluster (hardware barrier.cluster,
+//    ~0.3 us). Supports, weights and the work vectors are replicated in every
+//    CTA's shared memory; a value computed by one CTA is stored into all 16
+//    copies through distributed shared memory, so a phase reads nothing but
+//    its factor rows from L2. Group scans use 4 targets per lane.
+//  * GlobalPath: all state in global memory (L2), team = the same cluster or
+//    a cooperative grid of one CTA per SM (large scans, n >= 1024).
+// Both keep the global copies (L, Li, y, supports, weights) current, so a
+// run can pause (RBF_EGROW) and resume in either path.
 #include <cooperative_groups.h>
 
 #include <cmath>
@@ -39,20 +44,24 @@ namespace rbf {
 constexpr int kLoopThreads = 512;
 constexpr int kLoopWarps = kLoopThreads / 32;
 constexpr int kClusterCTAs = 16;
-constexpr int kSupTile = 2048;       // supports staged per scan tile (SoA, 96 KB)
-constexpr int kRowSmemMax = 8192;    // row held in shared memory (64 KB)
+constexpr int kSupTile = 2048;       // GlobalPath: supports staged per scan tile
+constexpr int kRowSmemMax = 8192;    // GlobalPath: row held in shared memory
+constexpr int kSmallMax = 1024;      // SmemPath: supports resident in shared memory
 constexpr int kAutoClusterMaxCard = 2048;
+constexpr int kNone = 0x7fffffff;
 
 struct LoopScratch {
   unsigned* bar;   // grid barrier word
   int* fault;
-  Best* part;      // [ctas][2]: unrestricted, eligible-only
+  Best* part;      // [2 parities][ctas][2]: unrestricted, eligible-only
   double* red;     // [ctas][4]: c.c, c.y(3)
   double* err;     // [nb]   errors of the group being scanned
   double* dmin;    // [nb]   seed farthest-point distances
   double* c0;      // [cap]
   double* r;       // [cap]
   double* c1;      // [cap]
+  double* gpt;     // [nb][3] boundary points in group order
+  double* gdisp;   // [nb][3] displacements in group order
 };
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
@@ -69,13 +78,15 @@ static LoopScratch carve(void* base, int nb, int cap, int ctas, size_t* total) {
   char* b = take(64);
   s.bar = reinterpret_cast<unsigned*>(b);
   s.fault = reinterpret_cast<int*>(b ? b + 32 : nullptr);
-  s.part = reinterpret_cast<Best*>(take(sizeof(Best) * 2 * ctas));
+  s.part = reinterpret_cast<Best*>(take(sizeof(Best) * 4 * ctas));
   s.red = reinterpret_cast<double*>(take(sizeof(double) * 4 * ctas));
   s.err = reinterpret_cast<double*>(take(sizeof(double) * (size_t)nb));
   s.dmin = reinterpret_cast<double*>(take(sizeof(double) * (size_t)nb));
   s.c0 = reinterpret_cast<double*>(take(sizeof(double) * (size_t)cap));
   s.r = reinterpret_cast<double*>(take(sizeof(double) * (size_t)cap));
   s.c1 = reinterpret_cast<double*>(take(sizeof(double) * (size_t)cap));
+  s.gpt = reinterpret_cast<double*>(take(sizeof(double) * 3 * (size_t)nb));
+  s.gdisp = reinterpret_cast<double*>(take(sizeof(double) * 3 * (size_t)nb));
   if (total) *total = off;
   return s;
 }
@@ -103,8 +114,9 @@ struct GridTeam {
       while (((old ^ ld_acquire(word)) & 0x80000000u) == 0) {
         if ((++spins & 1023u) == 0) {
           const uint64_t now = globaltimer_ns();
-          if (t0 == 0) t0 = now;
-          else if (now - t0 > 20ull * 1000000000ull) {
+          if (t0 == 0) {
+            t0 = now;
+          } else if (now - t0 > 20ull * 1000000000ull) {
             atomicExch(fault, 1);
             __trap();
           }
@@ -115,19 +127,8 @@ struct GridTeam {
   }
 };
 
-struct Shared {
-  double sx[kSupTile], sy[kSupTile], sz[kSupTile];
-  double wx[kSupTile], wy[kSupTile], wz[kSupTile];
-  double red[kLoopWarps * 32 * 4];
-  Best wb[kLoopWarps][2];
-  double wred[kLoopWarps][4];
-  Best bcast[2];
-  double dbl[8];
-  double phase[12];
-};
-
-// CTA 0's SM clock at phase boundaries (diagnostics in rbf_gcb_state)
-// (thread 0 of CTA 0 only; accumulators live in shared memory)
+// CTA 0's SM clock at phase boundaries (diagnostics in rbf_gcb_state),
+// kept by thread 0 of CTA 0 in shared memory.
 struct PhaseClock {
   double* acc;
   long long last;
@@ -156,172 +157,31 @@ __device__ __forceinline__ uint64_t leader_timer() {
   return (blockIdx.x == 0 && threadIdx.x == 0) ? globaltimer_ns() : 0ull;
 }
 
-// Fold per-warp bests into one per CTA (thread 0 of warp 0 ends with it).
-__device__ __forceinline__ void cta_best(Shared& sh, Best b, int slot, Best* out) {
+// Per-CTA small shared state common to both paths.
+struct Common {
+  double red[kLoopWarps * 32 * 4];
+  Best wb[kLoopWarps][2];
+  double wred[kLoopWarps][4];
+  Best bcast[2];
+  double dbl[8];
+  double phase[12];
+};
+
+// Fold per-warp bests; every lane of warp 0 ends with the CTA's best.
+__device__ __forceinline__ Best cta_best(Common& cm, Best b, int slot) {
   b = warp_best(b);
-  if ((threadIdx.x & 31) == 0) sh.wb[threadIdx.x >> 5][slot] = b;
+  if ((threadIdx.x & 31) == 0) cm.wb[threadIdx.x >> 5][slot] = b;
   __syncthreads();
+  Best v{-1.0, kNone};
   if (threadIdx.x < 32) {
-    Best v = threadIdx.x < kLoopWarps ? sh.wb[threadIdx.x][slot] : Best{-1.0, 0x7fffffff};
+    v = threadIdx.x < kLoopWarps ? cm.wb[threadIdx.x][slot] : Best{-1.0, kNone};
     v = warp_best(v);
-    if (threadIdx.x == 0) *out = v;
   }
+  return v;
 }
 
-// All CTAs fold the per-CTA partials (G <= 148) in the same fixed tree order.
-__device__ __forceinline__ void fold_partials(const LoopScratch& s, Shared& sh, int nslots) {
-  const int G = gridDim.x;
-  if (threadIdx.x < 32 * nslots) {
-    const int slot = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    Best b{-1.0, 0x7fffffff};
-#pragma unroll
-    for (int q = 0; q < 5; ++q) {
-      const int c = lane + 32 * q;
-      if (c < G) {
-        const Best v{__ldcg(&s.part[2 * c + slot].err), __ldcg(&s.part[2 * c + slot].pos)};
-        b = best_of(b, v);
-      }
-    }
-    b = warp_best(b);
-    if (lane == 0) sh.bcast[slot] = b;
-  }
-  __syncthreads();
-}
-
-// ------------------------------------------------------------------ scan
-// Errors of `card` boundary rows (positions gpos[t], or t when gpos is null)
-// against the n supports; writes err[t] and this CTA's two arg-max partials.
-// The team's CTAs split the rows; inside a CTA, S lanes share one row and
-// split its supports (S chosen so the rows fill the CTA), supports are
-// staged through shared memory in SoA tiles.
-__device__ void scan_phase(const rbf_gcb_args& a, const LoopScratch& s, Shared& sh,
-                           const int* gpos, int card, int n, double inv_r) {
-  const int tid = threadIdx.x, G = gridDim.x;
-  const int lo = (int)((int64_t)card * blockIdx.x / G);
-  const int hi = (int)((int64_t)card * (blockIdx.x + 1) / G);
-  const int mine = hi - lo;
-  int S = 32;
-  while (S > 1 && mine * S > kLoopThreads) S >>= 1;
-  while (S > 1 && (S >> 1) >= n) S >>= 1;
-  const int groups = kLoopThreads / S;
-  const int g = tid / S, sub = tid % S;
-  const int rounds = (mine + groups - 1) / groups;
-  const double* gx = a.sup;
-  const int cap = a.cap;
-
-  Best bu{-1.0, 0x7fffffff}, br{-1.0, 0x7fffffff};
-  for (int rd = 0; rd < rounds; ++rd) {
-    const int t = lo + rd * groups + g;
-    const bool active = t < hi;
-    int pos = 0;
-    double px = 0.0, py = 0.0, pz = 0.0;
-    if (active) {
-      pos = gpos ? __ldg(gpos + t) : t;
-      px = __ldg(a.points + 3 * (int64_t)pos) * inv_r;
-      py = __ldg(a.points + 3 * (int64_t)pos + 1) * inv_r;
-      pz = __ldg(a.points + 3 * (int64_t)pos + 2) * inv_r;
-    }
-    double ax = 0.0, ay = 0.0, az = 0.0;
-    for (int t0 = 0; t0 < n; t0 += kSupTile) {
-      const int cnt = min(kSupTile, n - t0);
-      if (rd == 0 || n > kSupTile) {
-        __syncthreads();
-        for (int j = tid; j < cnt; j += kLoopThreads) {
-          sh.sx[j] = __ldcg(gx + t0 + j) * inv_r;
-          sh.sy[j] = __ldcg(gx + cap + t0 + j) * inv_r;
-          sh.sz[j] = __ldcg(gx + 2 * cap + t0 + j) * inv_r;
-          sh.wx[j] = __ldcg(gx + 3 * cap + t0 + j);
-          sh.wy[j] = __ldcg(gx + 4 * cap + t0 + j);
-          sh.wz[j] = __ldcg(gx + 5 * cap + t0 + j);
-        }
-        __syncthreads();
-      }
-      if (active) {
-#pragma unroll 4
-        for (int j = sub; j < cnt; j += S)
-          pair_accum(px, py, pz, sh.sx[j], sh.sy[j], sh.sz[j], sh.wx[j], sh.wy[j], sh.wz[j], ax, ay,
-                     az);
-      }
-    }
-    for (int off = S >> 1; off > 0; off >>= 1) {
-      ax += __shfl_xor_sync(0xffffffffu, ax, off);
-      ay += __shfl_xor_sync(0xffffffffu, ay, off);
-      az += __shfl_xor_sync(0xffffffffu, az, off);
-    }
-    if (active && sub == 0) {
-      const double e = residual_norm(__ldg(a.disp + 3 * (int64_t)pos), __ldg(a.disp + 3 * (int64_t)pos + 1),
-                                     __ldg(a.disp + 3 * (int64_t)pos + 2), ax, ay, az);
-      s.err[t] = e;
-      if (better(e, pos, bu.err, bu.pos)) bu = Best{e, pos};
-      if (!__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + pos) && better(e, pos, br.err, br.pos))
-        br = Best{e, pos};
-    }
-  }
-  cta_best(sh, bu, 0, &s.part[2 * blockIdx.x]);
-  cta_best(sh, br, 1, &s.part[2 * blockIdx.x + 1]);
-}
-
-// Next candidate after a rejection: eligible arg-max over the stored group
-// errors (rare path; every CTA scans the whole group redundantly).
-__device__ Best rescan_candidate(const rbf_gcb_args& a, const LoopScratch& s, Shared& sh,
-                                 const int* gpos, int card) {
-  Best b{-1.0, 0x7fffffff};
-  for (int t = threadIdx.x; t < card; t += kLoopThreads) {
-    const int pos = gpos ? __ldg(gpos + t) : t;
-    if (__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + pos)) continue;
-    const double e = __ldcg(s.err + t);
-    if (better(e, pos, b.err, b.pos)) b = Best{e, pos};
-  }
-  __syncthreads();
-  cta_best(sh, b, 1, &sh.bcast[1]);
-  __syncthreads();
-  return sh.bcast[1];
-}
-
-// ------------------------------------------------------------------ seeds
-// selection.py:198-212: argmax |d| (first occurrence), then twice
-// argmax dmin with dmin = min(dmin, |P - P_next|); norms are
-// sqrt((x0*x0 + x1*x1) + x2*x2), numpy's bits for a (n, 3) row norm.
-template <class Team>
-__device__ void device_seeds(const rbf_gcb_args& a, const LoopScratch& s, Shared& sh,
-                             const Team& team, int seeds[3]) {
-  const int nb = a.nb, G = gridDim.x;
-  const int lo = (int)((int64_t)nb * blockIdx.x / G), hi = (int)((int64_t)nb * (blockIdx.x + 1) / G);
-  Best b{-1.0, 0x7fffffff};
-  for (int i = lo + threadIdx.x; i < hi; i += kLoopThreads) {
-    const double m = residual_norm(__ldg(a.disp + 3 * (int64_t)i), __ldg(a.disp + 3 * (int64_t)i + 1),
-                                   __ldg(a.disp + 3 * (int64_t)i + 2), 0.0, 0.0, 0.0);
-    if (better(m, i, b.err, b.pos)) b = Best{m, i};
-  }
-  cta_best(sh, b, 0, &s.part[2 * blockIdx.x]);
-  team.sync();
-  fold_partials(s, sh, 1);
-  seeds[0] = sh.bcast[0].pos;
-  for (int q = 1; q < 3; ++q) {
-    const int p = seeds[q - 1];
-    const double qx = __ldg(a.points + 3 * (int64_t)p), qy = __ldg(a.points + 3 * (int64_t)p + 1),
-                 qz = __ldg(a.points + 3 * (int64_t)p + 2);
-    Best bb{-1.0, 0x7fffffff};
-    for (int i = lo + threadIdx.x; i < hi; i += kLoopThreads) {
-      double d = residual_norm(__ldg(a.points + 3 * (int64_t)i), __ldg(a.points + 3 * (int64_t)i + 1),
-                               __ldg(a.points + 3 * (int64_t)i + 2), qx, qy, qz);
-      if (q == 2) d = fmin(s.dmin[i], d);
-      s.dmin[i] = d;
-      if (better(d, i, bb.err, bb.pos)) bb = Best{d, i};
-    }
-    __syncthreads();
-    cta_best(sh, bb, 0, &s.part[2 * blockIdx.x]);
-    team.sync();
-    fold_partials(s, sh, 1);
-    seeds[q] = sh.bcast[0].pos;
-  }
-}
-
-// ------------------------------------------------------------------ append
-enum AppendResult { kAccepted = 0, kRejectDup = 1, kRejectPivot = 2 };
-
-// Warp-cooperative dot product of packed row i of A with x[0..i], every load
-// of the lane issued before the first FMA (8 in flight per lane).
+// Warp-cooperative dot product of packed row `arow` (len entries) with x,
+// every load of the lane issued before the first FMA (8 in flight per lane).
 template <typename XL>
 __device__ __forceinline__ double row_dot(const double* arow, int len, XL xload, int lane) {
   double acc = 0.0;
@@ -339,148 +199,594 @@ __device__ __forceinline__ double row_dot(const double* arow, int len, XL xload,
   return warp_sum(acc);
 }
 
-// Bordered append of boundary position `pos` (reference core.py:153-185 via
-// selection.py:288-297 / 341-356). All CTAs call it; the result is uniform.
-template <class Team>
-__device__ int append_node(const rbf_gcb_args& a, const LoopScratch& s, Shared& sh, double* row,
-                           const Team& team, int pos, int& n, bool check_dup, double inv_r,
-                           double* pivot2_out, PhaseClock& pc) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int G = gridDim.x;
-  const double px = __ldg(a.points + 3 * (int64_t)pos), py = __ldg(a.points + 3 * (int64_t)pos + 1),
-               pz = __ldg(a.points + 3 * (int64_t)pos + 2);
-  // row[j] = phi(cdist(p, s_j) / R) with the reference's rounding; min distance
+enum AppendResult { kAccepted = 0, kRejectDup = 1, kRejectPivot = 2 };
+
+// The reference's seed row distance and kernel value for candidate p vs the
+// n supports, min distance block-reduced (every CTA computes the full row).
+template <typename PL>
+__device__ __forceinline__ double exact_row(Common& cm, double* row, int n, double px, double py,
+                                            double pz, double radius, PL sup_xyz) {
   double dmin = INFINITY;
-  for (int j = tid; j < n; j += kLoopThreads) {
-    const double d = cdist_exact(px, py, pz, __ldcg(a.sup + j), __ldcg(a.sup + a.cap + j),
-                                 __ldcg(a.sup + 2 * (int64_t)a.cap + j));
-    row[j] = phi_exact(d, a.radius);
+  for (int j = threadIdx.x; j < n; j += kLoopThreads) {
+    double sx, sy, sz;
+    sup_xyz(j, sx, sy, sz);
+    const double d = cdist_exact(px, py, pz, sx, sy, sz);
+    row[j] = phi_exact(d, radius);
     dmin = fmin(dmin, d);
   }
   dmin = warp_min(dmin);
-  if (lane == 0) sh.wred[warp][0] = dmin;
+  if ((threadIdx.x & 31) == 0) cm.wred[threadIdx.x >> 5][0] = dmin;
   __syncthreads();
-  if (tid < 32) {
-    double m = tid < kLoopWarps ? sh.wred[tid][0] : INFINITY;
+  if (threadIdx.x < 32) {
+    double m = threadIdx.x < kLoopWarps ? cm.wred[threadIdx.x][0] : INFINITY;
     m = warp_min(m);
-    if (tid == 0) sh.dbl[0] = m;
+    if (threadIdx.x == 0) cm.dbl[0] = m;
   }
   __syncthreads();
-  if (check_dup && n > 0 && sh.dbl[0] < a.dup_dist) return kRejectDup;
-
-  pc.mark(1);
-  const int gw = blockIdx.x * kLoopWarps + warp, nw = G * kLoopWarps;
-  // c0 = Li row
-  for (int i = gw; i < n; i += nw) {
-    const double v = row_dot(a.Li + tri_off(i), i + 1, [&](int j) { return row[j]; }, lane);
-    if (lane == 0) s.c0[i] = v;
-  }
-  team.sync();
-  pc.mark(2);
-  // r = row - L c0
-  for (int i = gw; i < n; i += nw) {
-    const double v = row_dot(a.L + tri_off(i), i + 1, [&](int j) { return __ldcg(s.c0 + j); }, lane);
-    if (lane == 0) s.r[i] = row[i] - v;
-  }
-  team.sync();
-  pc.mark(3);
-  // c = c0 + Li r, with per-warp partial sums of c.c and c.y
-  double pcc = 0.0, pcy0 = 0.0, pcy1 = 0.0, pcy2 = 0.0;
-  for (int i = gw; i < n; i += nw) {
-    const double v = row_dot(a.Li + tri_off(i), i + 1, [&](int j) { return __ldcg(s.r + j); }, lane);
-    if (lane == 0) {
-      const double c = __ldcg(s.c0 + i) + v;
-      s.c1[i] = c;
-      pcc = fma(c, c, pcc);
-      pcy0 = fma(c, __ldcg(a.y + 3 * (int64_t)i), pcy0);
-      pcy1 = fma(c, __ldcg(a.y + 3 * (int64_t)i + 1), pcy1);
-      pcy2 = fma(c, __ldcg(a.y + 3 * (int64_t)i + 2), pcy2);
-    }
-  }
-  if (lane == 0) {
-    sh.wred[warp][0] = pcc;
-    sh.wred[warp][1] = pcy0;
-    sh.wred[warp][2] = pcy1;
-    sh.wred[warp][3] = pcy2;
-  }
-  __syncthreads();
-  if (tid < 4) {
-    double t = 0.0;
-    for (int w = 0; w < kLoopWarps; ++w) t += sh.wred[w][tid];
-    s.red[4 * blockIdx.x + tid] = t;
-  }
-  team.sync();
-  pc.mark(4);
-  // every CTA folds the G partials with the same fixed tree
-  if (tid < 128) {
-    const int q = tid >> 5, ln = tid & 31;
-    double t = 0.0;
-#pragma unroll
-    for (int u = 0; u < 5; ++u) {
-      const int c = ln + 32 * u;
-      if (c < G) t += __ldcg(s.red + 4 * c + q);
-    }
-    t = warp_sum(t);
-    if (ln == 0) sh.dbl[1 + q] = t;
-  }
-  __syncthreads();
-  const double pivot2 = 1.0 - sh.dbl[1];  // row[n] = phi(0) = 1 exactly
-  *pivot2_out = pivot2;
-  if (!(pivot2 > 0.0)) {
-    __syncthreads();
-    return kRejectPivot;
-  }
-  const double l = sqrt(pivot2);
-  const double yn0 = (__ldg(a.disp + 3 * (int64_t)pos) - sh.dbl[2]) / l;
-  const double yn1 = (__ldg(a.disp + 3 * (int64_t)pos + 1) - sh.dbl[3]) / l;
-  const double yn2 = (__ldg(a.disp + 3 * (int64_t)pos + 2) - sh.dbl[4]) / l;
-  // u = Li^T c, v = Li^T y -> new Li row, new L row, refreshed weights
-  double* Lrow = a.L + tri_off(n);
-  double* Lirow = a.Li + tri_off(n);
-  double* wgt = a.sup + 3 * (int64_t)a.cap;
-  const int cap = a.cap;
-  tri_cols<4, kLoopWarps>(
-      a.Li, n,
-      [&](int i, int c) { return c == 0 ? __ldcg(s.c1 + i) : __ldcg(a.y + 3 * (int64_t)i + (c - 1)); },
-      (int)blockIdx.x, G, sh.red, [&](int j, const double* sum) {
-        const double lij = -sum[0] / l;
-        Lirow[j] = lij;
-        Lrow[j] = __ldcg(s.c1 + j);
-        wgt[j] = fma(lij, yn0, sum[1]);
-        wgt[cap + j] = fma(lij, yn1, sum[2]);
-        wgt[2 * cap + j] = fma(lij, yn2, sum[3]);
-      });
-  if (blockIdx.x == 0 && tid == 0) {
-    Lirow[n] = 1.0 / l;
-    Lrow[n] = l;
-    a.y[3 * (int64_t)n] = yn0;
-    a.y[3 * (int64_t)n + 1] = yn1;
-    a.y[3 * (int64_t)n + 2] = yn2;
-    a.sup[n] = px;
-    a.sup[cap + n] = py;
-    a.sup[2 * cap + n] = pz;
-    wgt[n] = yn0 / l;
-    wgt[cap + n] = yn1 / l;
-    wgt[2 * cap + n] = yn2 / l;
-    a.sel[n] = pos;
-  }
-  if (tid == 0) a.inel[pos] = 1;
-  n += 1;
-  team.sync();
-  pc.mark(5);
-  return kAccepted;
+  return cm.dbl[0];
 }
 
-// ------------------------------------------------------------------ kernel
+// ================================================================ GlobalPath
+struct GlobalShared {
+  Common cm;
+  double sx[kSupTile], sy[kSupTile], sz[kSupTile];
+  double wx[kSupTile], wy[kSupTile], wz[kSupTile];
+  double row[kRowSmemMax];
+};
+
 template <class Team>
-__device__ void gcb_body(const rbf_gcb_args& a, const LoopScratch& s, const Team& team) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
-  double* row = reinterpret_cast<double*>(smem_raw + sizeof(Shared));
+struct GlobalPath {
+  const rbf_gcb_args& a;
+  const LoopScratch& s;
+  GlobalShared& sh;
+  Team team;
+  double inv_r;
+  PhaseClock& pc;
+
+  static constexpr int kMaxN = kRowSmemMax;
+  __device__ Common& cm() { return sh.cm; }
+  __device__ void sync() { team.sync(); }
+  __device__ void begin(int /*n*/) {}
+
+  // this CTA's partial -> global, double-buffered by parity
+  __device__ void publish(Best b, int slot, int par) {
+    if (threadIdx.x == 0) s.part[(par * gridDim.x + blockIdx.x) * 2 + slot] = b;
+  }
+  __device__ void fold(int par, int nslots) {
+    const int G = gridDim.x;
+    if (threadIdx.x < 32 * nslots) {
+      const int slot = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      Best b{-1.0, kNone};
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        const int c = lane + 32 * q;
+        if (c < G) {
+          const Best* p = &s.part[(par * G + c) * 2 + slot];
+          b = best_of(b, Best{__ldcg(&p->err), __ldcg(&p->pos)});
+        }
+      }
+      b = warp_best(b);
+      if (lane == 0) sh.cm.bcast[slot] = b;
+    }
+    __syncthreads();
+  }
+
+  // errors of `card` rows; the team's CTAs split the rows, S lanes share a row
+  __device__ void scan(const int* gpos, const double* gpt, const double* gdisp, int card, int n,
+                       int par) {
+    const int tid = threadIdx.x, G = gridDim.x;
+    const int lo = (int)((int64_t)card * blockIdx.x / G);
+    const int hi = (int)((int64_t)card * (blockIdx.x + 1) / G);
+    const int mine = hi - lo;
+    int S = 32;
+    while (S > 1 && mine * S > kLoopThreads) S >>= 1;
+    while (S > 1 && (S >> 1) >= n) S >>= 1;
+    const int groups = kLoopThreads / S;
+    const int g = tid / S, sub = tid % S;
+    const int rounds = (mine + groups - 1) / groups;
+    const double* gx = a.sup;
+    const int cap = a.cap;
+    Best bu{-1.0, kNone}, br{-1.0, kNone};
+    for (int rd = 0; rd < rounds; ++rd) {
+      const int t = lo + rd * groups + g;
+      const bool active = t < hi;
+      int pos = 0;
+      double px = 0.0, py = 0.0, pz = 0.0;
+      bool elig = false;
+      if (active) {
+        pos = gpos ? __ldg(gpos + t) : t;
+        px = __ldcg(gpt + 3 * (int64_t)t) * inv_r;
+        py = __ldcg(gpt + 3 * (int64_t)t + 1) * inv_r;
+        pz = __ldcg(gpt + 3 * (int64_t)t + 2) * inv_r;
+        elig = !__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + pos);
+      }
+      double ax = 0.0, ay = 0.0, az = 0.0;
+      for (int t0 = 0; t0 < n; t0 += kSupTile) {
+        const int cnt = min(kSupTile, n - t0);
+        if (rd == 0 || n > kSupTile) {
+          __syncthreads();
+          for (int j = tid; j < cnt; j += kLoopThreads) {
+            sh.sx[j] = __ldcg(gx + t0 + j) * inv_r;
+            sh.sy[j] = __ldcg(gx + cap + t0 + j) * inv_r;
+            sh.sz[j] = __ldcg(gx + 2 * cap + t0 + j) * inv_r;
+            sh.wx[j] = __ldcg(gx + 3 * cap + t0 + j);
+            sh.wy[j] = __ldcg(gx + 4 * cap + t0 + j);
+            sh.wz[j] = __ldcg(gx + 5 * cap + t0 + j);
+          }
+          __syncthreads();
+        }
+        if (active) {
+#pragma unroll 4
+          for (int j = sub; j < cnt; j += S)
+            pair_accum(px, py, pz, sh.sx[j], sh.sy[j], sh.sz[j], sh.wx[j], sh.wy[j], sh.wz[j], ax,
+                       ay, az);
+        }
+      }
+      for (int off = S >> 1; off > 0; off >>= 1) {
+        ax += __shfl_xor_sync(0xffffffffu, ax, off);
+        ay += __shfl_xor_sync(0xffffffffu, ay, off);
+        az += __shfl_xor_sync(0xffffffffu, az, off);
+      }
+      if (active && sub == 0) {
+        const double e = residual_norm(__ldcg(gdisp + 3 * (int64_t)t), __ldcg(gdisp + 3 * (int64_t)t + 1),
+                                       __ldcg(gdisp + 3 * (int64_t)t + 2), ax, ay, az);
+        s.err[t] = e;
+        if (better(e, pos, bu.err, bu.pos)) bu = Best{e, pos};
+        if (elig && better(e, pos, br.err, br.pos)) br = Best{e, pos};
+      }
+    }
+    publish(cta_best(sh.cm, bu, 0), 0, par);
+    publish(cta_best(sh.cm, br, 1), 1, par);
+  }
+
+  __device__ int append(int pos, int& n, bool check_dup, double* pivot2_out) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x;
+    const int cap = a.cap;
+    const double px = __ldg(a.points + 3 * (int64_t)pos), py = __ldg(a.points + 3 * (int64_t)pos + 1),
+                 pz = __ldg(a.points + 3 * (int64_t)pos + 2);
+    double* row = sh.row;
+    const double dmin = exact_row(sh.cm, row, n, px, py, pz, a.radius, [&](int j, double& x, double& y, double& z) {
+      x = __ldcg(a.sup + j);
+      y = __ldcg(a.sup + cap + j);
+      z = __ldcg(a.sup + 2 * (int64_t)cap + j);
+    });
+    if (check_dup && n > 0 && dmin < a.dup_dist) return kRejectDup;
+    pc.mark(1);
+    const int gw = blockIdx.x * kLoopWarps + warp, nw = G * kLoopWarps;
+    for (int i = gw; i < n; i += nw) {  // c0 = Li row
+      const double v = row_dot(a.Li + tri_off(i), i + 1, [&](int j) { return row[j]; }, lane);
+      if (lane == 0) s.c0[i] = v;
+    }
+    team.sync();
+    pc.mark(2);
+    for (int i = gw; i < n; i += nw) {  // r = row - L c0
+      const double v = row_dot(a.L + tri_off(i), i + 1, [&](int j) { return __ldcg(s.c0 + j); }, lane);
+      if (lane == 0) s.r[i] = row[i] - v;
+    }
+    team.sync();
+    pc.mark(3);
+    double pcc = 0.0, pcy0 = 0.0, pcy1 = 0.0, pcy2 = 0.0;
+    for (int i = gw; i < n; i += nw) {  // c = c0 + Li r
+      const double v = row_dot(a.Li + tri_off(i), i + 1, [&](int j) { return __ldcg(s.r + j); }, lane);
+      if (lane == 0) {
+        const double c = __ldcg(s.c0 + i) + v;
+        s.c1[i] = c;
+        pcc = fma(c, c, pcc);
+        pcy0 = fma(c, __ldcg(a.y + 3 * (int64_t)i), pcy0);
+        pcy1 = fma(c, __ldcg(a.y + 3 * (int64_t)i + 1), pcy1);
+        pcy2 = fma(c, __ldcg(a.y + 3 * (int64_t)i + 2), pcy2);
+      }
+    }
+    Common& cm = sh.cm;
+    if (lane == 0) {
+      cm.wred[warp][0] = pcc;
+      cm.wred[warp][1] = pcy0;
+      cm.wred[warp][2] = pcy1;
+      cm.wred[warp][3] = pcy2;
+    }
+    __syncthreads();
+    if (tid < 4) {
+      double t = 0.0;
+      for (int w = 0; w < kLoopWarps; ++w) t += cm.wred[w][tid];
+      s.red[4 * blockIdx.x + tid] = t;
+    }
+    team.sync();
+    pc.mark(4);
+    if (tid < 128) {  // every CTA folds the G partials with the same tree
+      const int q = tid >> 5, ln = tid & 31;
+      double t = 0.0;
+#pragma unroll
+      for (int u = 0; u < 5; ++u) {
+        const int c = ln + 32 * u;
+        if (c < G) t += __ldcg(s.red + 4 * c + q);
+      }
+      t = warp_sum(t);
+      if (ln == 0) cm.dbl[1 + q] = t;
+    }
+    __syncthreads();
+    const double pivot2 = 1.0 - cm.dbl[1];  // row[n] = phi(0) = 1 exactly
+    *pivot2_out = pivot2;
+    if (!(pivot2 > 0.0)) {
+      __syncthreads();
+      return kRejectPivot;
+    }
+    const double l = sqrt(pivot2);
+    const double yn0 = (__ldg(a.disp + 3 * (int64_t)pos) - cm.dbl[2]) / l;
+    const double yn1 = (__ldg(a.disp + 3 * (int64_t)pos + 1) - cm.dbl[3]) / l;
+    const double yn2 = (__ldg(a.disp + 3 * (int64_t)pos + 2) - cm.dbl[4]) / l;
+    double* Lrow = a.L + tri_off(n);
+    double* Lirow = a.Li + tri_off(n);
+    double* wgt = a.sup + 3 * (int64_t)cap;
+    tri_cols<4, kLoopWarps>(
+        a.Li, n,
+        [&](int i, int c) { return c == 0 ? __ldcg(s.c1 + i) : __ldcg(a.y + 3 * (int64_t)i + (c - 1)); },
+        (int)blockIdx.x, G, cm.red, [&](int j, const double* sum) {
+          const double lij = -sum[0] / l;
+          Lirow[j] = lij;
+          Lrow[j] = __ldcg(s.c1 + j);
+          wgt[j] = fma(lij, yn0, sum[1]);
+          wgt[cap + j] = fma(lij, yn1, sum[2]);
+          wgt[2 * cap + j] = fma(lij, yn2, sum[3]);
+        });
+    if (blockIdx.x == 0 && tid == 0) {
+      Lirow[n] = 1.0 / l;
+      Lrow[n] = l;
+      a.y[3 * (int64_t)n] = yn0;
+      a.y[3 * (int64_t)n + 1] = yn1;
+      a.y[3 * (int64_t)n + 2] = yn2;
+      a.sup[n] = px;
+      a.sup[cap + n] = py;
+      a.sup[2 * cap + n] = pz;
+      wgt[n] = yn0 / l;
+      wgt[cap + n] = yn1 / l;
+      wgt[2 * cap + n] = yn2 / l;
+      a.sel[n] = pos;
+    }
+    if (tid == 0) a.inel[pos] = 1;
+    n += 1;
+    team.sync();
+    pc.mark(5);
+    return kAccepted;
+  }
+};
+
+// ================================================================= SmemPath
+struct SmemShared {
+  Common cm;
+  double ux[kSmallMax], uy[kSmallMax], uz[kSmallMax];  // support coordinates
+  double sx[kSmallMax], sy[kSmallMax], sz[kSmallMax];  // ... scaled by 1/R
+  double wx[kSmallMax], wy[kSmallMax], wz[kSmallMax];  // weights
+  double y0[kSmallMax], y1[kSmallMax], y2[kSmallMax];  // forward-substituted d
+  double row[kSmallMax], c0[kSmallMax], r[kSmallMax], c1[kSmallMax];
+  Best part[2][kClusterCTAs][2];  // scan partials, written by every CTA (DSMEM)
+  double rpart[kClusterCTAs][4];  // c.c, c.y partials (DSMEM)
+};
+
+struct SmemPath {
+  const rbf_gcb_args& a;
+  const LoopScratch& s;
+  SmemShared& sh;
+  double inv_r;
+  PhaseClock& pc;
+
+  static constexpr int kMaxN = kSmallMax;
+  static constexpr int kTPT = 4;  // targets per lane in group scans
+  __device__ Common& cm() { return sh.cm; }
+  __device__ void sync() { cg::this_cluster().sync(); }
+
+  // pointer to the same shared-memory object in CTA `rank` of the cluster
+  template <typename T>
+  __device__ __forceinline__ T* at(T* p, int rank) {
+    return cg::this_cluster().map_shared_rank(p, rank);
+  }
+
+  // load the resident copies from the global state (every launch)
+  __device__ void begin(int n) {
+    const int cap = a.cap;
+    for (int j = threadIdx.x; j < n; j += kLoopThreads) {
+      const double x = __ldcg(a.sup + j), y = __ldcg(a.sup + cap + j), z = __ldcg(a.sup + 2 * cap + j);
+      sh.ux[j] = x;
+      sh.uy[j] = y;
+      sh.uz[j] = z;
+      sh.sx[j] = x * inv_r;
+      sh.sy[j] = y * inv_r;
+      sh.sz[j] = z * inv_r;
+      sh.wx[j] = __ldcg(a.sup + 3 * cap + j);
+      sh.wy[j] = __ldcg(a.sup + 4 * cap + j);
+      sh.wz[j] = __ldcg(a.sup + 5 * cap + j);
+      sh.y0[j] = __ldcg(a.y + 3 * j);
+      sh.y1[j] = __ldcg(a.y + 3 * j + 1);
+      sh.y2[j] = __ldcg(a.y + 3 * j + 2);
+    }
+    __syncthreads();
+  }
+
+  // lanes 0..15 of warp 0 (which all hold b) store it into every CTA's slot
+  __device__ void publish(Best b, int slot, int par) {
+    if (threadIdx.x < kClusterCTAs) *at(&sh.part[par][blockIdx.x][slot], (int)threadIdx.x) = b;
+  }
+  __device__ void fold(int par, int nslots) {
+    if (threadIdx.x < 32 * nslots) {
+      const int slot = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      Best b = lane < kClusterCTAs ? sh.part[par][lane][slot] : Best{-1.0, kNone};
+      b = warp_best(b);
+      if (lane == 0) sh.cm.bcast[slot] = b;
+    }
+    __syncthreads();
+  }
+
+  __device__ void scan(const int* gpos, const double* gpt, const double* gdisp, int card, int n,
+                       int par) {
+    const int tid = threadIdx.x;
+    const int lo = (int)((int64_t)card * blockIdx.x / kClusterCTAs);
+    const int hi = (int)((int64_t)card * (blockIdx.x + 1) / kClusterCTAs);
+    const int tgroups = (hi - lo + kTPT - 1) / kTPT;
+    int S = 32;
+    while (S > 1 && tgroups * S > kLoopThreads) S >>= 1;
+    while (S > 1 && (S >> 1) >= n) S >>= 1;
+    const int per_round = kLoopThreads / S;
+    const int rounds = (tgroups + per_round - 1) / per_round;
+    const int sub = tid % S;
+    Best bu{-1.0, kNone}, br{-1.0, kNone};
+    for (int rd = 0; rd < rounds; ++rd) {
+      const int tg = rd * per_round + tid / S;
+      double px[kTPT], py[kTPT], pz[kTPT], ax[kTPT], ay[kTPT], az[kTPT];
+      int pos[kTPT];
+      bool elig[kTPT];
+#pragma unroll
+      for (int q = 0; q < kTPT; ++q) {
+        const int t = lo + kTPT * tg + q;
+        const bool ok = tg < tgroups && t < hi;
+        pos[q] = ok ? (gpos ? __ldg(gpos + t) : t) : -1;
+        px[q] = ok ? __ldcg(gpt + 3 * (int64_t)t) * inv_r : 0.0;
+        py[q] = ok ? __ldcg(gpt + 3 * (int64_t)t + 1) * inv_r : 0.0;
+        pz[q] = ok ? __ldcg(gpt + 3 * (int64_t)t + 2) * inv_r : 0.0;
+        ax[q] = ay[q] = az[q] = 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < kTPT; ++q)
+        elig[q] = pos[q] >= 0 && !__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + pos[q]);
+      if (tg < tgroups) {
+#pragma unroll 1
+        for (int j = sub; j < n; j += S) {
+          const double sx = sh.sx[j], sy = sh.sy[j], sz = sh.sz[j];
+          const double wx = sh.wx[j], wy = sh.wy[j], wz = sh.wz[j];
+#pragma unroll
+          for (int q = 0; q < kTPT; ++q)
+            pair_accum(px[q], py[q], pz[q], sx, sy, sz, wx, wy, wz, ax[q], ay[q], az[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kTPT; ++q) {
+        for (int off = S >> 1; off > 0; off >>= 1) {
+          ax[q] += __shfl_xor_sync(0xffffffffu, ax[q], off);
+          ay[q] += __shfl_xor_sync(0xffffffffu, ay[q], off);
+          az[q] += __shfl_xor_sync(0xffffffffu, az[q], off);
+        }
+      }
+      if (sub == 0) {
+#pragma unroll
+        for (int q = 0; q < kTPT; ++q) {
+          if (pos[q] < 0) continue;
+          const int t = lo + kTPT * tg + q;
+          const double e = residual_norm(__ldcg(gdisp + 3 * (int64_t)t), __ldcg(gdisp + 3 * (int64_t)t + 1),
+                                         __ldcg(gdisp + 3 * (int64_t)t + 2), ax[q], ay[q], az[q]);
+          s.err[t] = e;
+          if (better(e, pos[q], bu.err, bu.pos)) bu = Best{e, pos[q]};
+          if (elig[q] && better(e, pos[q], br.err, br.pos)) br = Best{e, pos[q]};
+        }
+      }
+    }
+    publish(cta_best(sh.cm, bu, 0), 0, par);
+    publish(cta_best(sh.cm, br, 1), 1, par);
+  }
+
+  __device__ int append(int pos, int& n, bool check_dup, double* pivot2_out) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rank = blockIdx.x;
+    const int cap = a.cap;
+    const double px = __ldg(a.points + 3 * (int64_t)pos), py = __ldg(a.points + 3 * (int64_t)pos + 1),
+                 pz = __ldg(a.points + 3 * (int64_t)pos + 2);
+    const double dmin = exact_row(sh.cm, sh.row, n, px, py, pz, a.radius,
+                                  [&](int j, double& x, double& y, double& z) {
+                                    x = sh.ux[j];
+                                    y = sh.uy[j];
+                                    z = sh.uz[j];
+                                  });
+    if (check_dup && n > 0 && dmin < a.dup_dist) return kRejectDup;
+    pc.mark(1);
+    const int gw = rank * kLoopWarps + warp, nw = kClusterCTAs * kLoopWarps;
+    // c0 = Li row; each value stored into all 16 CTAs by lanes 0..15
+    for (int i = gw; i < n; i += nw) {
+      const double v = row_dot(a.Li + tri_off(i), i + 1, [&](int j) { return sh.row[j]; }, lane);
+      if (lane < kClusterCTAs) *at(&sh.c0[i], lane) = v;
+    }
+    sync();
+    pc.mark(2);
+    for (int i = gw; i < n; i += nw) {  // r = row - L c0
+      const double v = row_dot(a.L + tri_off(i), i + 1, [&](int j) { return sh.c0[j]; }, lane);
+      if (lane < kClusterCTAs) *at(&sh.r[i], lane) = sh.row[i] - v;
+    }
+    sync();
+    pc.mark(3);
+    double pcc = 0.0, pcy0 = 0.0, pcy1 = 0.0, pcy2 = 0.0;
+    for (int i = gw; i < n; i += nw) {  // c = c0 + Li r
+      const double v = row_dot(a.Li + tri_off(i), i + 1, [&](int j) { return sh.r[j]; }, lane);
+      const double c = sh.c0[i] + v;
+      if (lane < kClusterCTAs) *at(&sh.c1[i], lane) = c;
+      if (lane == 0) {
+        a.L[tri_off(n) + i] = c;  // row n of L (global)
+        pcc = fma(c, c, pcc);
+        pcy0 = fma(c, sh.y0[i], pcy0);
+        pcy1 = fma(c, sh.y1[i], pcy1);
+        pcy2 = fma(c, sh.y2[i], pcy2);
+      }
+    }
+    Common& cm = sh.cm;
+    if (lane == 0) {
+      cm.wred[warp][0] = pcc;
+      cm.wred[warp][1] = pcy0;
+      cm.wred[warp][2] = pcy1;
+      cm.wred[warp][3] = pcy2;
+    }
+    __syncthreads();
+    if (tid < 4) {
+      double t = 0.0;
+      for (int w = 0; w < kLoopWarps; ++w) t += cm.wred[w][tid];
+      for (int c = 0; c < kClusterCTAs; ++c) *at(&sh.rpart[rank][tid], c) = t;
+    }
+    sync();
+    pc.mark(4);
+    if (tid < 4) {  // fixed-order fold of the 16 CTA partials
+      double t = 0.0;
+      for (int c = 0; c < kClusterCTAs; ++c) t += sh.rpart[c][tid];
+      cm.dbl[1 + tid] = t;
+    }
+    __syncthreads();
+    const double pivot2 = 1.0 - cm.dbl[1];  // row[n] = phi(0) = 1 exactly
+    *pivot2_out = pivot2;
+    if (!(pivot2 > 0.0)) {
+      __syncthreads();
+      return kRejectPivot;
+    }
+    const double l = sqrt(pivot2);
+    const double yn0 = (__ldg(a.disp + 3 * (int64_t)pos) - cm.dbl[2]) / l;
+    const double yn1 = (__ldg(a.disp + 3 * (int64_t)pos + 1) - cm.dbl[3]) / l;
+    const double yn2 = (__ldg(a.disp + 3 * (int64_t)pos + 2) - cm.dbl[4]) / l;
+    double* Lirow = a.Li + tri_off(n);
+    double* wgt = a.sup + 3 * (int64_t)cap;
+    tri_cols<4, kLoopWarps>(
+        a.Li, n,
+        [&](int i, int c) { return c == 0 ? sh.c1[i] : (c == 1 ? sh.y0[i] : (c == 2 ? sh.y1[i] : sh.y2[i])); },
+        rank, kClusterCTAs, cm.red, [&](int j, const double* sum) {
+          const double lij = -sum[0] / l;
+          const double w0 = fma(lij, yn0, sum[1]), w1 = fma(lij, yn1, sum[2]), w2 = fma(lij, yn2, sum[3]);
+          Lirow[j] = lij;
+          wgt[j] = w0;
+          wgt[cap + j] = w1;
+          wgt[2 * cap + j] = w2;
+          for (int c = 0; c < kClusterCTAs; ++c) {
+            *at(&sh.wx[j], c) = w0;
+            *at(&sh.wy[j], c) = w1;
+            *at(&sh.wz[j], c) = w2;
+          }
+        });
+    if (tid == 0) {  // the new support, in every CTA's resident copy
+      sh.ux[n] = px;
+      sh.uy[n] = py;
+      sh.uz[n] = pz;
+      sh.sx[n] = px * inv_r;
+      sh.sy[n] = py * inv_r;
+      sh.sz[n] = pz * inv_r;
+      sh.wx[n] = yn0 / l;
+      sh.wy[n] = yn1 / l;
+      sh.wz[n] = yn2 / l;
+      sh.y0[n] = yn0;
+      sh.y1[n] = yn1;
+      sh.y2[n] = yn2;
+      a.inel[pos] = 1;
+      if (rank == 0) {  // and in the global state
+        Lirow[n] = 1.0 / l;
+        a.L[tri_off(n) + n] = l;
+        a.y[3 * (int64_t)n] = yn0;
+        a.y[3 * (int64_t)n + 1] = yn1;
+        a.y[3 * (int64_t)n + 2] = yn2;
+        a.sup[n] = px;
+        a.sup[cap + n] = py;
+        a.sup[2 * cap + n] = pz;
+        wgt[n] = yn0 / l;
+        wgt[cap + n] = yn1 / l;
+        wgt[2 * cap + n] = yn2 / l;
+        a.sel[n] = pos;
+      }
+    }
+    n += 1;
+    sync();
+    pc.mark(5);
+    return kAccepted;
+  }
+};
+
+// ================================================================== driver
+// Next candidate after a rejection: eligible arg-max over the stored group
+// errors (rare path; every CTA scans the whole group redundantly).
+__device__ Best rescan_candidate(const rbf_gcb_args& a, const LoopScratch& s, Common& cm,
+                                 const int* gpos, int card) {
+  Best b{-1.0, kNone};
+  for (int t = threadIdx.x; t < card; t += kLoopThreads) {
+    const int pos = gpos ? __ldg(gpos + t) : t;
+    if (__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + pos)) continue;
+    const double e = __ldcg(s.err + t);
+    if (better(e, pos, b.err, b.pos)) b = Best{e, pos};
+  }
+  __syncthreads();
+  b = cta_best(cm, b, 1);
+  if (threadIdx.x == 0) cm.bcast[1] = b;
+  __syncthreads();
+  return cm.bcast[1];
+}
+
+// Gather the boundary into group order (gpt/gdisp), once per launch.
+__device__ void gather_groups(const rbf_gcb_args& a, const LoopScratch& s) {
+  const int G = gridDim.x;
+  for (int t = blockIdx.x * kLoopThreads + threadIdx.x; t < a.nb; t += G * kLoopThreads) {
+    const int p = __ldg(a.group_pos + t);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      s.gpt[3 * (int64_t)t + c] = __ldg(a.points + 3 * (int64_t)p + c);
+      s.gdisp[3 * (int64_t)t + c] = __ldg(a.disp + 3 * (int64_t)p + c);
+    }
+  }
+}
+
+// selection.py:198-212: argmax |d| (first occurrence), then twice
+// argmax dmin with dmin = min(dmin, |P - P_next|); norms are
+// sqrt((x0*x0 + x1*x1) + x2*x2), numpy's bits for a (n, 3) row norm.
+template <class Path>
+__device__ void device_seeds(Path& P, const rbf_gcb_args& a, const LoopScratch& s, int seeds[3],
+                             int& par) {
+  const int nb = a.nb, G = gridDim.x;
+  const int lo = (int)((int64_t)nb * blockIdx.x / G), hi = (int)((int64_t)nb * (blockIdx.x + 1) / G);
+  Best b{-1.0, kNone};
+  for (int i = lo + threadIdx.x; i < hi; i += kLoopThreads) {
+    const double m = residual_norm(__ldg(a.disp + 3 * (int64_t)i), __ldg(a.disp + 3 * (int64_t)i + 1),
+                                   __ldg(a.disp + 3 * (int64_t)i + 2), 0.0, 0.0, 0.0);
+    if (better(m, i, b.err, b.pos)) b = Best{m, i};
+  }
+  P.publish(cta_best(P.cm(), b, 0), 0, par);
+  P.sync();
+  P.fold(par, 1);
+  par ^= 1;
+  seeds[0] = P.cm().bcast[0].pos;
+  for (int q = 1; q < 3; ++q) {
+    const int p = seeds[q - 1];
+    const double qx = __ldg(a.points + 3 * (int64_t)p), qy = __ldg(a.points + 3 * (int64_t)p + 1),
+                 qz = __ldg(a.points + 3 * (int64_t)p + 2);
+    Best bb{-1.0, kNone};
+    for (int i = lo + threadIdx.x; i < hi; i += kLoopThreads) {
+      double d = residual_norm(__ldg(a.points + 3 * (int64_t)i), __ldg(a.points + 3 * (int64_t)i + 1),
+                               __ldg(a.points + 3 * (int64_t)i + 2), qx, qy, qz);
+      if (q == 2) d = fmin(s.dmin[i], d);
+      s.dmin[i] = d;
+      if (better(d, i, bb.err, bb.pos)) bb = Best{d, i};
+    }
+    __syncthreads();
+    P.publish(cta_best(P.cm(), bb, 0), 0, par);
+    P.sync();
+    P.fold(par, 1);
+    par ^= 1;
+    seeds[q] = P.cm().bcast[0].pos;
+  }
+}
+
+template <class Path>
+__device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s, PhaseClock& pc,
+                           int self_mode) {
   const int tid = threadIdx.x;
   const bool leader = blockIdx.x == 0 && tid == 0;
-  const double inv_r = 1.0 / a.radius;
   rbf_gcb_state* st = a.state;
+  Common& cm = P.cm();
 
   int n = __ldcg(&st->n);
   int k = __ldcg(&st->k);
@@ -490,12 +796,11 @@ __device__ void gcb_body(const rbf_gcb_args& a, const LoopScratch& s, const Team
   int done_loop = __ldcg(&st->done_loop);
   double t2_carry = __ldcg(&st->t2_carry);
   const int m = a.m;
+  int par = 0;
 
-  PhaseClock pc;
-  pc.start(sh.phase);
-  auto save = [&](int status) {
+  auto save = [&](int status, int want_mode) {
     if (leader) {
-      for (int i = 0; i < 12; ++i) st->phase_cycles[i] += sh.phase[i];
+      for (int i = 0; i < 12; ++i) st->phase_cycles[i] += cm.phase[i];
       st->n = n;
       st->k = k;
       st->streak_ok = streak_ok;
@@ -503,28 +808,33 @@ __device__ void gcb_body(const rbf_gcb_args& a, const LoopScratch& s, const Team
       st->n_records = nrec;
       st->done_loop = done_loop;
       st->t2_carry = t2_carry;
+      st->want_mode = want_mode;
       st->status = status;
     }
   };
 
+  gather_groups(a, s);
+  P.begin(n);
+  P.sync();
+
   if (n == 0) {
     if (a.cap < 3 || a.rec_cap < 1) {
-      save(RBF_EGROW);
+      save(RBF_EGROW, self_mode);
       return;
     }
     int seeds[3];
-    device_seeds(a, s, sh, team, seeds);
+    device_seeds(P, a, s, seeds, par);
     pc.mark(7);
     // seed appends (selection.py:288-297): no near-duplicate guard, NotPD propagates
     for (int q = 0; q < 3; ++q) {
       double p2 = 0.0;
-      const int res = append_node(a, s, sh, row, team, seeds[q], n, false, inv_r, &p2, pc);
+      const int res = P.append(seeds[q], n, false, &p2);
       if (res != kAccepted) {
         if (leader) {
           st->fail_row = n;
           st->fail_pivot2 = p2;
         }
-        save(RBF_ENOTPD);
+        save(RBF_ENOTPD, self_mode);
         return;
       }
     }
@@ -539,8 +849,12 @@ __device__ void gcb_body(const rbf_gcb_args& a, const LoopScratch& s, const Team
       done_loop = 1;
       break;
     }
-    if (n >= a.cap || nrec >= a.rec_cap || n >= kRowSmemMax) {
-      save(RBF_EGROW);
+    if (n >= Path::kMaxN - 1) {  // beyond this path's resident capacity
+      save(RBF_EGROW, self_mode == RBF_GCB_SMEM ? RBF_GCB_CLUSTER : self_mode);
+      return;
+    }
+    if (n >= a.cap || nrec >= a.rec_cap) {
+      save(RBF_EGROW, self_mode);
       return;
     }
     const uint64_t t_a = leader_timer();
@@ -549,22 +863,23 @@ __device__ void gcb_body(const rbf_gcb_args& a, const LoopScratch& s, const Team
     const int card = __ldg(a.group_off + gi + 1) - off;
     const int* gpos = a.group_pos + off;
     pc.mark(6);
-    scan_phase(a, s, sh, gpos, card, n, inv_r);
-    team.sync();
+    P.scan(gpos, s.gpt + 3 * (int64_t)off, s.gdisp + 3 * (int64_t)off, card, n, par);
+    P.sync();
     pc.mark(0);
     pc.count(10);
-    fold_partials(s, sh, 2);
-    const Best bu = sh.bcast[0];
-    Best cand = sh.bcast[1];
+    P.fold(par, 2);
+    par ^= 1;
+    const Best bu = cm.bcast[0];
+    Best cand = cm.bcast[1];
     const uint64_t t_b = leader_timer();
     const int n_before = n;
     const double local_max = bu.err;
     bool added = false;
     int added_pos = -1;
     if (local_max > a.tol) {
-      while (cand.pos != 0x7fffffff && cand.err > a.tol) {
+      while (cand.pos != kNone && cand.err > a.tol) {
         double p2;
-        const int res = append_node(a, s, sh, row, team, cand.pos, n, true, inv_r, &p2, pc);
+        const int res = P.append(cand.pos, n, true, &p2);
         pc.count(9);
         if (res == kAccepted) {
           added = true;
@@ -576,7 +891,7 @@ __device__ void gcb_body(const rbf_gcb_args& a, const LoopScratch& s, const Team
           __threadfence();
         }
         __syncthreads();
-        cand = rescan_candidate(a, s, sh, gpos, card);
+        cand = rescan_candidate(a, s, cm, gpos, card);
       }
     }
     const uint64_t t_c = leader_timer();
@@ -601,7 +916,7 @@ __device__ void gcb_body(const rbf_gcb_args& a, const LoopScratch& s, const Team
         break;
       }
       if (streak_noadd >= m) {
-        save(RBF_ESTALL);
+        save(RBF_ESTALL, self_mode);
         return;
       }
     } else {
@@ -611,18 +926,19 @@ __device__ void gcb_body(const rbf_gcb_args& a, const LoopScratch& s, const Team
     k += 1;
   }
 
-  // final verification sweep (selection.py:388-412)
+  // final verification sweep (selection.py:388-412), natural order
   if (nrec >= a.rec_cap) {
-    save(RBF_EGROW);
+    save(RBF_EGROW, self_mode);
     return;
   }
   const uint64_t t_a = leader_timer();
   pc.mark(6);
-  scan_phase(a, s, sh, nullptr, a.nb, n, inv_r);
-  team.sync();
-  fold_partials(s, sh, 1);
+  P.scan(nullptr, a.points, a.disp, a.nb, n, par);
+  P.sync();
+  P.fold(par, 1);
+  par ^= 1;
   pc.mark(8);
-  const Best bu = sh.bcast[0];
+  const Best bu = cm.bcast[0];
   const uint64_t t_b = leader_timer();
   if (leader) {
     rbf_gcb_record rec;
@@ -638,23 +954,62 @@ __device__ void gcb_body(const rbf_gcb_args& a, const LoopScratch& s, const Team
     st->final_pos = bu.pos;
   }
   nrec += 1;
-  save(1);
+  save(1, self_mode);
+}
+
+extern __shared__ __align__(16) unsigned char g_smem[];
+
+template <class Team>
+__device__ void run_global(const rbf_gcb_args& a, const LoopScratch& s, Team team, int mode) {
+  GlobalShared& sh = *reinterpret_cast<GlobalShared*>(g_smem);
+  PhaseClock pc;
+  pc.start(sh.cm.phase);
+  GlobalPath<Team> P{a, s, sh, team, 1.0 / a.radius, pc};
+  gcb_driver(P, a, s, pc, mode);
 }
 
 __global__ void __launch_bounds__(kLoopThreads, 1) gcb_cluster_kernel(rbf_gcb_args a, LoopScratch s) {
-  gcb_body(a, s, ClusterTeam{});
+  run_global(a, s, ClusterTeam{}, RBF_GCB_CLUSTER);
 }
 
 __global__ void __launch_bounds__(kLoopThreads, 1) gcb_grid_kernel(rbf_gcb_args a, LoopScratch s) {
-  gcb_body(a, s, GridTeam{s.bar, s.fault});
+  run_global(a, s, GridTeam{s.bar, s.fault}, RBF_GCB_GRID);
 }
 
-static size_t loop_smem_bytes() { return sizeof(Shared) + (size_t)kRowSmemMax * sizeof(double); }
+__global__ void __launch_bounds__(kLoopThreads, 1) gcb_smem_kernel(rbf_gcb_args a, LoopScratch s) {
+  SmemShared& sh = *reinterpret_cast<SmemShared*>(g_smem);
+  PhaseClock pc;
+  pc.start(sh.cm.phase);
+  SmemPath P{a, s, sh, 1.0 / a.radius, pc};
+  gcb_driver(P, a, s, pc, RBF_GCB_SMEM);
+}
 
 static int resolve_mode(int mode, int nb, int m) {
   if (mode != RBF_GCB_AUTO) return mode;
   const int card = (nb + m - 1) / m;
-  return card <= kAutoClusterMaxCard ? RBF_GCB_CLUSTER : RBF_GCB_GRID;
+  return card <= kAutoClusterMaxCard ? RBF_GCB_SMEM : RBF_GCB_GRID;
+}
+
+static cudaError_t launch_cluster(const void* fn, rbf_gcb_args& a, LoopScratch& s, size_t smem,
+                                  cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kClusterCTAs);
+  cfg.blockDim = dim3(kLoopThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kClusterCTAs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  void* args[] = {&a, &s};
+  return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 }  // namespace rbf
@@ -672,12 +1027,14 @@ extern "C" int rbf_device_info(int device, int* sm_count_host, int* loop_ctas_ho
 extern "C" int rbf_gcb_ctas(int32_t mode, int32_t nb, int32_t m, int32_t* ctas_host,
                             int32_t* resolved_mode_host) {
   if (nb < 1 || m < 1) return set_error(RBF_EARG, "bad nb/m");
+  if (mode < RBF_GCB_AUTO || mode > RBF_GCB_SMEM) return set_error(RBF_EARG, "bad mode %d", mode);
   int dev = 0;
   RBF_CUDA_TRY(cudaGetDevice(&dev));
   const int r = resolve_mode(mode, nb, m);
   const int sms = sm_count(dev);
   if (sms <= 0) return set_error(RBF_ECUDA, "no CUDA device");
-  if (ctas_host) *ctas_host = r == RBF_GCB_CLUSTER ? kClusterCTAs : sms;
+  // scratch is sized for the widest team so a run can switch paths
+  if (ctas_host) *ctas_host = r == RBF_GCB_GRID ? sms : kClusterCTAs;
   if (resolved_mode_host) *resolved_mode_host = r;
   return RBF_OK;
 }
@@ -705,25 +1062,13 @@ extern "C" int rbf_gcb_run(const rbf_gcb_args* args, void* stream) {
     return set_error(RBF_EARG, "scratch too small (%zu < %zu)", a.scratch_bytes, need);
   cudaStream_t st = as_stream(stream);
   RBF_CUDA_TRY(cudaMemsetAsync(s.bar, 0, 64, st));
-  const size_t smem = loop_smem_bytes();
   rbf_gcb_args acopy = a;
-  if (mode == RBF_GCB_CLUSTER) {
-    RBF_CUDA_TRY(cudaFuncSetAttribute(gcb_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    RBF_CUDA_TRY(cudaFuncSetAttribute(gcb_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kClusterCTAs);
-    cfg.blockDim = dim3(kLoopThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = kClusterCTAs;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    RBF_CUDA_TRY(cudaLaunchKernelEx(&cfg, gcb_cluster_kernel, acopy, s));
+  if (mode == RBF_GCB_SMEM) {
+    RBF_CUDA_TRY(launch_cluster((const void*)gcb_smem_kernel, acopy, s, sizeof(SmemShared), st));
+  } else if (mode == RBF_GCB_CLUSTER) {
+    RBF_CUDA_TRY(launch_cluster((const void*)gcb_cluster_kernel, acopy, s, sizeof(GlobalShared), st));
   } else {
+    const size_t smem = sizeof(GlobalShared);
     RBF_CUDA_TRY(cudaFuncSetAttribute(gcb_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     void* kargs[] = {&acopy, &s};
     RBF_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)gcb_grid_kernel, dim3(ctas), dim3(kLoopThreads),

@@ -53,11 +53,12 @@ __device__ __forceinline__ void tri_cols(const double* A, int n, XL xload, int s
     double acc[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) acc[c] = 0.0;
-    // 8 rows per batch: every load of the batch is issued before its FMAs
-    for (int i0 = 32 * J + warp; i0 < n; i0 += 8 * NW) {
-      double av[8], xv[8][K];
+    // U rows per batch: every load of the batch is issued before its FMAs
+    constexpr int U = K >= 4 ? 4 : 8;
+    for (int i0 = 32 * J + warp; i0 < n; i0 += U * NW) {
+      double av[U], xv[U][K];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int i = i0 + u * NW;
         const bool ok = i < n && j <= i;
         av[u] = ok ? __ldcg(A + tri_off(i) + j) : 0.0;
@@ -65,7 +66,7 @@ __device__ __forceinline__ void tri_cols(const double* A, int n, XL xload, int s
         for (int c = 0; c < K; ++c) xv[u][c] = (i < n) ? xload(i, c) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < U; ++u) {
 #pragma unroll
         for (int c = 0; c < K; ++c) acc[c] = fma(av[u], xv[u][c], acc[c]);
       }

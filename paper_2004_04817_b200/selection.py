@@ -299,6 +299,12 @@ class _LoopBuffers:
         self.scratch_bytes = lib.rbf_gcb_scratch_bytes(self.nb, cap, self.ctas)
         self.scratch = t.empty(self.scratch_bytes, dtype=t.uint8, device=dev)
 
+    def resize_scratch(self, ctas):
+        self.ctas = ctas
+        lib = N.load()
+        self.scratch_bytes = lib.rbf_gcb_scratch_bytes(self.nb, self.cap, ctas)
+        self.scratch = self.t.empty(self.scratch_bytes, dtype=self.t.uint8, device=self.dev)
+
     def _grow_records(self, rec_cap, nrec):
         t = self.t
         rec = t.empty((rec_cap, N.RECORD_DTYPE.itemsize), dtype=t.uint8, device=self.dev)
@@ -385,10 +391,17 @@ def _gcb_run(boundary, config, mode=None):
             )
         if st.status != N.RBF_EGROW:
             raise N.NativeUnavailableError(f"selection kernel ended with status {st.status}")
+        if st.want_mode != args.mode:
+            # the shared-memory path is full: resume in the L2-resident path
+            N.check(lib.rbf_gcb_ctas(st.want_mode, nb, m, N.ctypes.byref(ctas),
+                                     N.ctypes.byref(resolved)), "rbf_gcb_ctas")
+            args.mode = resolved.value
+            buf.resize_scratch(ctas.value)
+            continue
+        if st.n >= _DEVICE_MAX_SUPPORTS - 1:
+            raise N.NativeUnavailableError(
+                f"support count exceeds the device loop limit ({_DEVICE_MAX_SUPPORTS - 1})")
         if st.n >= buf.cap:
-            if st.n >= _DEVICE_MAX_SUPPORTS:
-                raise N.NativeUnavailableError(
-                    f"support count exceeds the device loop limit ({_DEVICE_MAX_SUPPORTS})")
             buf._grow_factor(max(min(2 * buf.cap, limit, _DEVICE_MAX_SUPPORTS), st.n + 1), st.n)
         if st.n_records >= buf.rec_cap:
             buf._grow_records(2 * buf.rec_cap, st.n_records)
@@ -435,7 +448,7 @@ def _gcb_run(boundary, config, mode=None):
     )
     # diagnostics: SM cycles of CTA 0 per phase of the device loop
     history.device_phase_cycles = dict(zip(N.PHASES, list(st.phase_cycles)))
-    history.device_mode = "cluster" if args.mode == N.GCB_CLUSTER else "grid"
+    history.device_mode = {N.GCB_CLUSTER: "cluster", N.GCB_GRID: "grid", N.GCB_SMEM: "smem"}[args.mode]
     support = SupportSet(nodes=idx[sel], points=boundary.points[sel], weights=weights)
     return SelectionResult(
         support=support, history=history, converged=float(fin["local_max"]) <= config.tol

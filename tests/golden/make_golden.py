@@ -107,6 +107,14 @@ def main():
             out, _ = run_selection(pts, disp, 3.0, 1e-4, min(len(pts), 80), m, seed)
             save(f"smooth{seed}_m{m}", points=pts, disp=disp, **out)
 
+    # a run long enough (n = 1200) to cross the shared-memory path's capacity
+    rng = np.random.default_rng(77)
+    pts = rng.uniform(0, 1, (4000, 3))
+    disp = np.stack([0.05 * np.sin(4 * pts[:, 0] + 1), 0.05 * np.cos(3 * pts[:, 1]),
+                     0.05 * np.sin(5 * pts[:, 2] + pts[:, 0])], 1)
+    out, _ = run_selection(pts, disp, 0.25, 1e-7, 1200, 8, 3)
+    save("switch_m8", points=pts, disp=disp, **out)
+
     # 2. evaluation and factor known answers
     rng = np.random.default_rng(1234)
     sp = rng.normal(size=(700, 3))

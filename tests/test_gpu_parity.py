@@ -222,6 +222,7 @@ GOLDEN_SELECTIONS = [
     ("hemisphere_m1", 1e-9), ("hemisphere_m4", 1e-9), ("smooth0_m1", 1e-9), ("smooth0_m5", 1e-9),
     ("smooth3_m1", 1e-9), ("smooth3_m5", 1e-9), ("smooth11_m1", 1e-9), ("smooth11_m5", 1e-9),
     ("cfg0_m1", 1e-9), ("cfg0_m8", 1e-9), ("cfg1_m32", 1e-9), ("cfg2s_m48", 2e-8),
+    ("switch_m8", 1e-9),  # n = 1200: crosses from the shared-memory path to the L2 path
 ]
 
 
@@ -373,9 +374,9 @@ def test_estimator_drop_in(cuda, rng):
 
 @pytest.mark.parametrize("name", ["cfg0_m8", "cfg0_m1", "smooth0_m5", "hemisphere_m4"])
 def test_selection_cluster_and_grid_modes(cuda, name):
-    """Both launch shapes of the loop kernel (one 16-CTA cluster with
-    hardware barriers; a cooperative grid of one CTA per SM) reproduce the
-    reference sequence."""
+    """Every launch shape of the loop kernel (16-CTA cluster with
+    shared-memory-resident state; the same cluster with L2-resident state;
+    a cooperative grid of one CTA per SM) reproduces the reference."""
     from paper_2004_04817_b200 import _native as N
     from paper_2004_04817_b200.selection import _gcb_run
 
@@ -384,7 +385,7 @@ def test_selection_cluster_and_grid_modes(cuda, name):
     radius, tol, cap, m, seed = g["params"]
     b = cuda.BoundarySet(np.arange(len(pts)), pts, disp)
     cfg = cuda.SelectionConfig(radius=radius, tol=tol, max_supports=int(cap), m=int(m), seed=int(seed))
-    for mode in (N.GCB_CLUSTER, N.GCB_GRID):
+    for mode in (N.GCB_SMEM, N.GCB_CLUSTER, N.GCB_GRID):
         res = _gcb_run(b, cfg, mode=mode)
         assert np.array_equal(res.support.nodes, g["seq"]), mode
         assert [r.node for r in res.history.records] == g["rec_node"].tolist()

@@ -34,6 +34,29 @@ __global__ void chase_kernel(const int* next, int steps, unsigned long long* out
   sink[0] = p;
 }
 
+__global__ void timer_kernel(unsigned long long* out, int iters) {
+  unsigned long long acc = 0;
+  long long c0 = clock64();
+  for (int i = 0; i < iters; ++i) acc += rbf::globaltimer_ns();
+  long long c1 = clock64();
+  for (int i = 0; i < iters; ++i) acc += clock64();
+  long long c2 = clock64();
+  out[6] = (unsigned long long)(c1 - c0);
+  out[7] = (unsigned long long)(c2 - c1) + (acc & 1);
+}
+
+// DSMEM: each CTA stores 1 double into every CTA of the cluster, then syncs
+__global__ void dsmem_kernel(int iters, unsigned long long* out) {
+  __shared__ double buf[16];
+  cg::cluster_group c = cg::this_cluster();
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    if (threadIdx.x < 16) *c.map_shared_rank(&buf[blockIdx.x % 16], threadIdx.x) = (double)i;
+    c.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[4] = (unsigned long long)(clock64() - t0);
+}
+
 int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   rbf::GridBarrier* bar; int* fault; unsigned long long* out;
@@ -55,6 +78,16 @@ int main() {
     cudaError_t e = cudaLaunchKernelEx(&cfg, cluster_bar_kernel, iters, out, slot);
     if (e != cudaSuccess) printf("cluster %d launch: %s\n", cs, cudaGetErrorString(e));
   }
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(16); cfg.blockDim = dim3(512);
+    cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 16; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    cudaFuncSetAttribute(dsmem_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchKernelEx(&cfg, dsmem_kernel, iters, out);
+  }
+  timer_kernel<<<1, 1>>>(out, 1000);
   int n = 1 << 16; int* next; cudaMalloc(&next, n * 4);
   int* h = new int[n]; for (int i = 0; i < n; ++i) h[i] = (i * 7919 + 13) % n;
   cudaMemcpy(next, h, n * 4, cudaMemcpyHostToDevice);
@@ -68,5 +101,8 @@ int main() {
   printf("cluster barrier (8 CTAs):            %.3f us/barrier\n", r[2] / 1e3 / iters);
   printf("cluster barrier (16 CTAs):           %.3f us/barrier\n", r[3] / 1e3 / iters);
   printf("L2 dependent load latency:           %.1f ns\n", r[5] / 20000.0);
+  printf("DSMEM store x16 + cluster sync:      %.1f cycles\n", r[4] / (double)iters);
+  printf("globaltimer read:                    %.1f cycles\n", r[6] / 1000.0);
+  printf("clock64 read:                        %.1f cycles\n", r[7] / 1000.0);
   return 0;
 }
