@@ -268,7 +268,7 @@ def run_ours(args, rank, world, local):
 
     wl = workload(args.config)
     peak = measure_fp64_peak()
-    boundary = P.BoundarySet(np.arange(wl.nb), wl.points, wl.disp)
+    boundary = P.stage_boundary(P.BoundarySet(np.arange(wl.nb), wl.points, wl.disp))
     cfg = P.SelectionConfig(radius=wl.radius, tol=wl.tol, max_supports=wl.nb, m=wl.m, seed=wl.seed)
     lo, hi = multi.shard_range(wl.nv, rank, world)
     nv_local = hi - lo

@@ -160,19 +160,26 @@ typedef struct rbf_gcb_state {
   int32_t pad_;
   /* diagnostics: SM cycles CTA 0 spent per phase, summed over the run:
    * [0] scan+barrier, [1] fold+row, [2] c0, [3] r, [4] c, [5] pivot+cols,
-   * [6] bookkeeping, [7] seeds, [8] final sweep, [9] appends, [10] iterations */
-  double phase_cycles[12];
+   * [6] bookkeeping, [7] seeds, [8] final sweep, [9] appends, [10] iterations,
+   * [11..14] scan sub-phases: targets+compute, reduce, epilogue, partials,
+   * [15] column partials of Li^T [c, y] */
+  double phase_cycles[16];
 } rbf_gcb_state;
 
 /* Launch shapes of the selection kernel:
+ *  MSG     one 16-CTA cluster, n < 448: the factor rows (owner-stable, row
+ *          i in CTA i % 16) and all vectors resident in shared memory; every
+ *          cross-CTA value is pushed with st.async into the consumer's
+ *          mbarrier -- no cluster barriers in steady state;
  *  SMEM    one 16-CTA cluster; supports, weights and the Cholesky work
  *          vectors replicated in every CTA's shared memory (written through
  *          distributed shared memory), the factor rows in L2 (n < 1024);
  *  CLUSTER one 16-CTA cluster, all state in global memory (L2);
  *  GRID    one CTA per SM (cooperative), all state in global memory.
- * AUTO picks SMEM for group sizes up to 2048 (the kernel asks to resume in
- * CLUSTER once n reaches 1024) and GRID above. */
-enum { RBF_GCB_AUTO = 0, RBF_GCB_CLUSTER = 1, RBF_GCB_GRID = 2, RBF_GCB_SMEM = 3 };
+ * AUTO picks MSG for group sizes up to 2048 (the kernel asks to resume in
+ * SMEM once n reaches 448 and in CLUSTER once n reaches 1024) and GRID
+ * above. */
+enum { RBF_GCB_AUTO = 0, RBF_GCB_CLUSTER = 1, RBF_GCB_GRID = 2, RBF_GCB_SMEM = 3, RBF_GCB_MSG = 4 };
 
 typedef struct rbf_gcb_args {
   /* boundary (device) */

@@ -26,6 +26,7 @@ GCB_AUTO = 0
 GCB_CLUSTER = 1
 GCB_GRID = 2
 GCB_SMEM = 3
+GCB_MSG = 4
 
 c_dp = ctypes.c_void_p  # device pointers are passed as integers
 
@@ -66,13 +67,14 @@ class GcbState(ctypes.Structure):
         ("fault", ctypes.c_int32),
         ("want_mode", ctypes.c_int32),
         ("pad_", ctypes.c_int32),
-        ("phase_cycles", ctypes.c_double * 12),
+        ("phase_cycles", ctypes.c_double * 16),
     ]
 
 
-assert ctypes.sizeof(GcbState) == 168
+assert ctypes.sizeof(GcbState) == 200
 PHASES = ["scan", "fold_row", "c0", "r", "c", "pivot_cols", "bookkeeping", "seeds", "final_sweep",
-          "appends", "iterations"]
+          "appends", "iterations", "scan_compute", "scan_reduce", "scan_epilogue", "scan_partials",
+          "cols_partials"]
 
 
 class GcbArgs(ctypes.Structure):

@@ -137,7 +137,7 @@ struct PhaseClock {
     acc = smem_acc;
     on = blockIdx.x == 0 && threadIdx.x == 0;
     if (on) {
-      for (int i = 0; i < 12; ++i) acc[i] = 0.0;
+      for (int i = 0; i < 16; ++i) acc[i] = 0.0;
       last = clock64();
     }
   }
@@ -164,7 +164,7 @@ struct Common {
   double wred[kLoopWarps][4];
   Best bcast[2];
   double dbl[8];
-  double phase[12];
+  double phase[16];
 };
 
 // Fold per-warp bests; every lane of warp 0 ends with the CTA's best.
@@ -201,29 +201,26 @@ __device__ __forceinline__ double row_dot(const double* arow, int len, XL xload,
 
 enum AppendResult { kAccepted = 0, kRejectDup = 1, kRejectPivot = 2 };
 
-// The reference's seed row distance and kernel value for candidate p vs the
-// n supports, min distance block-reduced (every CTA computes the full row).
+// Row phi(cdist(p, s_j) / R) of candidate p against the n supports with the
+// reference's rounding (every CTA computes the full row), plus the
+// near-duplicate test min_j d_j < dup (selection.py:342-345) as a block-wide
+// flag.
 template <typename PL>
-__device__ __forceinline__ double exact_row(Common& cm, double* row, int n, double px, double py,
-                                            double pz, double radius, PL sup_xyz) {
-  double dmin = INFINITY;
+__device__ __forceinline__ bool exact_row(Common& cm, double* row, int n, double px, double py,
+                                          double pz, double radius, double dup, PL sup_xyz) {
+  if (threadIdx.x == 0) cm.dbl[0] = 0.0;
+  __syncthreads();
+  bool near = false;
   for (int j = threadIdx.x; j < n; j += kLoopThreads) {
     double sx, sy, sz;
     sup_xyz(j, sx, sy, sz);
     const double d = cdist_exact(px, py, pz, sx, sy, sz);
     row[j] = phi_exact(d, radius);
-    dmin = fmin(dmin, d);
+    near |= d < dup;
   }
-  dmin = warp_min(dmin);
-  if ((threadIdx.x & 31) == 0) cm.wred[threadIdx.x >> 5][0] = dmin;
+  if (__any_sync(0xffffffffu, near) && (threadIdx.x & 31) == 0) cm.dbl[0] = 1.0;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    double m = threadIdx.x < kLoopWarps ? cm.wred[threadIdx.x][0] : INFINITY;
-    m = warp_min(m);
-    if (threadIdx.x == 0) cm.dbl[0] = m;
-  }
-  __syncthreads();
-  return cm.dbl[0];
+  return cm.dbl[0] != 0.0;
 }
 
 // ================================================================ GlobalPath
@@ -247,11 +244,17 @@ struct GlobalPath {
   __device__ Common& cm() { return sh.cm; }
   __device__ void sync() { team.sync(); }
   __device__ void begin(int /*n*/) {}
+  __device__ int group_off(int g) { return __ldg(a.group_off + g); }
 
   // this CTA's partial -> global, double-buffered by parity
   __device__ void publish(Best b, int slot, int par) {
     if (threadIdx.x == 0) s.part[(par * gridDim.x + blockIdx.x) * 2 + slot] = b;
   }
+  __device__ void gather(int par, int nslots) {
+    team.sync();
+    fold(par, nslots);
+  }
+  __device__ void finish() {}
   __device__ void fold(int par, int nslots) {
     const int G = gridDim.x;
     if (threadIdx.x < 32 * nslots) {
@@ -346,12 +349,12 @@ struct GlobalPath {
     const double px = __ldg(a.points + 3 * (int64_t)pos), py = __ldg(a.points + 3 * (int64_t)pos + 1),
                  pz = __ldg(a.points + 3 * (int64_t)pos + 2);
     double* row = sh.row;
-    const double dmin = exact_row(sh.cm, row, n, px, py, pz, a.radius, [&](int j, double& x, double& y, double& z) {
+    const bool near = exact_row(sh.cm, row, n, px, py, pz, a.radius, a.dup_dist, [&](int j, double& x, double& y, double& z) {
       x = __ldcg(a.sup + j);
       y = __ldcg(a.sup + cap + j);
       z = __ldcg(a.sup + 2 * (int64_t)cap + j);
     });
-    if (check_dup && n > 0 && dmin < a.dup_dist) return kRejectDup;
+    if (check_dup && n > 0 && near) return kRejectDup;
     pc.mark(1);
     const int gw = blockIdx.x * kLoopWarps + warp, nw = G * kLoopWarps;
     for (int i = gw; i < n; i += nw) {  // c0 = Li row
@@ -452,6 +455,8 @@ struct GlobalPath {
 };
 
 // ================================================================= SmemPath
+constexpr int kGoffSmem = 4096;  // group offsets cached in shared memory
+
 struct SmemShared {
   Common cm;
   double ux[kSmallMax], uy[kSmallMax], uz[kSmallMax];  // support coordinates
@@ -459,9 +464,98 @@ struct SmemShared {
   double wx[kSmallMax], wy[kSmallMax], wz[kSmallMax];  // weights
   double y0[kSmallMax], y1[kSmallMax], y2[kSmallMax];  // forward-substituted d
   double row[kSmallMax], c0[kSmallMax], r[kSmallMax], c1[kSmallMax];
+  double colp[kSmallMax][4];      // this CTA's column partials of Li^T [c, y]
+  double acc[kLoopWarps][4][4];   // scan: per-warp reduced sums (4 targets x 3 comps)
+  int goff[kGoffSmem + 1];
   Best part[2][kClusterCTAs][2];  // scan partials, written by every CTA (DSMEM)
   double rpart[kClusterCTAs][4];  // c.c, c.y partials (DSMEM)
 };
+
+// Reduce-scatter butterfly over a full warp: v[16] per lane -> each value
+// summed over the 32 lanes with 16 shuffled doubles per lane (instead of 80
+// for independent xor trees). Returns the sum of value index `idx` (set on
+// return); lanes l and l^1 hold the same index.
+__device__ __forceinline__ double warp_reduce_scatter16(double (&v)[16], int lane, int& idx) {
+  int base = 0;
+#pragma unroll
+  for (int lev = 0; lev < 4; ++lev) {
+    const int off = 16 >> lev, half = 8 >> lev;
+    const bool hi = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double send = hi ? v[i] : v[i + half];
+      const double keep = hi ? v[i + half] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+    if (hi) base += half;
+  }
+  idx = base;
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+// Both arg-max partials of a CTA in one pass; every lane of warp 0 ends with
+// them. `lanes` = how many low lanes of each warp hold candidates (1..32).
+__device__ __forceinline__ void cta_best2(Common& cm, Best& bu, Best& br, int lanes) {
+  for (int off = 1; off < lanes; off <<= 1) {
+    const double eu = __shfl_xor_sync(0xffffffffu, bu.err, off);
+    const int pu = __shfl_xor_sync(0xffffffffu, bu.pos, off);
+    const double er = __shfl_xor_sync(0xffffffffu, br.err, off);
+    const int pr = __shfl_xor_sync(0xffffffffu, br.pos, off);
+    if (better(eu, pu, bu.err, bu.pos)) bu = Best{eu, pu};
+    if (better(er, pr, br.err, br.pos)) br = Best{er, pr};
+  }
+  if ((threadIdx.x & 31) == 0) {
+    cm.wb[threadIdx.x >> 5][0] = bu;
+    cm.wb[threadIdx.x >> 5][1] = br;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int l = threadIdx.x;
+    bu = l < kLoopWarps ? cm.wb[l][0] : Best{-1.0, kNone};
+    br = l < kLoopWarps ? cm.wb[l][1] : Best{-1.0, kNone};
+    for (int off = 1; off < kLoopWarps; off <<= 1) {
+      const double eu = __shfl_xor_sync(0xffffffffu, bu.err, off);
+      const int pu = __shfl_xor_sync(0xffffffffu, bu.pos, off);
+      const double er = __shfl_xor_sync(0xffffffffu, br.err, off);
+      const int pr = __shfl_xor_sync(0xffffffffu, br.pos, off);
+      if (better(eu, pu, bu.err, bu.pos)) bu = Best{eu, pu};
+      if (better(er, pr, br.err, br.pos)) br = Best{er, pr};
+    }
+  }
+}
+
+// Dot products of two packed rows (a: len_a entries, b: len_b) with x, the
+// two rows' elements dealt over the lanes as one list so that a short and a
+// long row together cost about one batch of loads.
+template <typename XL>
+__device__ __forceinline__ void row_dot_pair(const double* ra, int len_a, const double* rb, int len_b,
+                                             XL xload, int lane, double& sa, double& sb) {
+  constexpr int U = 12;
+  const int total = len_a + len_b;
+  double acc_a = 0.0, acc_b = 0.0;
+  for (int e0 = 0; e0 < total; e0 += U * kWarp) {
+    double av[U], xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * kWarp + lane;
+      const bool in_a = e < len_a;
+      const int j = in_a ? e : e - len_a;
+      const bool ok = e < total;
+      av[u] = ok ? __ldcg((in_a ? ra : rb) + j) : 0.0;
+      xv[u] = ok ? xload(j) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * kWarp + lane;
+      if (e < len_a)
+        acc_a = fma(av[u], xv[u], acc_a);
+      else
+        acc_b = fma(av[u], xv[u], acc_b);
+    }
+  }
+  sa = warp_sum(acc_a);
+  sb = warp_sum(acc_b);
+}
 
 struct SmemPath {
   const rbf_gcb_args& a;
@@ -499,13 +593,20 @@ struct SmemPath {
       sh.y1[j] = __ldcg(a.y + 3 * j + 1);
       sh.y2[j] = __ldcg(a.y + 3 * j + 2);
     }
+    for (int g = threadIdx.x; g <= a.m && g <= kGoffSmem; g += kLoopThreads) sh.goff[g] = __ldg(a.group_off + g);
     __syncthreads();
   }
+  __device__ int group_off(int g) { return a.m <= kGoffSmem ? sh.goff[g] : __ldg(a.group_off + g); }
 
   // lanes 0..15 of warp 0 (which all hold b) store it into every CTA's slot
   __device__ void publish(Best b, int slot, int par) {
     if (threadIdx.x < kClusterCTAs) *at(&sh.part[par][blockIdx.x][slot], (int)threadIdx.x) = b;
   }
+  __device__ void gather(int par, int nslots) {
+    sync();
+    fold(par, nslots);
+  }
+  __device__ void finish() {}
   __device__ void fold(int par, int nslots) {
     if (threadIdx.x < 32 * nslots) {
       const int slot = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -518,35 +619,44 @@ struct SmemPath {
 
   __device__ void scan(const int* gpos, const double* gpt, const double* gdisp, int card, int n,
                        int par) {
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
     const int lo = (int)((int64_t)card * blockIdx.x / kClusterCTAs);
     const int hi = (int)((int64_t)card * (blockIdx.x + 1) / kClusterCTAs);
     const int tgroups = (hi - lo + kTPT - 1) / kTPT;
     int S = 32;
     while (S > 1 && tgroups * S > kLoopThreads) S >>= 1;
-    while (S > 1 && (S >> 1) >= n) S >>= 1;
     const int per_round = kLoopThreads / S;
     const int rounds = (tgroups + per_round - 1) / per_round;
     const int sub = tid % S;
     Best bu{-1.0, kNone}, br{-1.0, kNone};
     for (int rd = 0; rd < rounds; ++rd) {
       const int tg = rd * per_round + tid / S;
-      double px[kTPT], py[kTPT], pz[kTPT], ax[kTPT], ay[kTPT], az[kTPT];
-      int pos[kTPT];
-      bool elig[kTPT];
+      double px[kTPT], py[kTPT], pz[kTPT];
+      double v[16];
 #pragma unroll
       for (int q = 0; q < kTPT; ++q) {
         const int t = lo + kTPT * tg + q;
         const bool ok = tg < tgroups && t < hi;
-        pos[q] = ok ? (gpos ? __ldg(gpos + t) : t) : -1;
         px[q] = ok ? __ldcg(gpt + 3 * (int64_t)t) * inv_r : 0.0;
         py[q] = ok ? __ldcg(gpt + 3 * (int64_t)t + 1) * inv_r : 0.0;
         pz[q] = ok ? __ldcg(gpt + 3 * (int64_t)t + 2) * inv_r : 0.0;
-        ax[q] = ay[q] = az[q] = 0.0;
+        v[4 * q] = v[4 * q + 1] = v[4 * q + 2] = v[4 * q + 3] = 0.0;
       }
-#pragma unroll
-      for (int q = 0; q < kTPT; ++q)
-        elig[q] = pos[q] >= 0 && !__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + pos[q]);
+      // the lane that finishes target q (lane q of the group when S == 32,
+      // else sub == 0) prefetches its position, eligibility and displacement
+      const int myq = S == 32 ? lane : 0;
+      const int my_t = lo + kTPT * tg + myq;
+      const bool mine = (S == 32 ? lane < kTPT : sub == 0) && tg < tgroups && my_t < hi;
+      int my_pos = -1;
+      bool my_elig = false;
+      double dx = 0.0, dy = 0.0, dz = 0.0;
+      if (mine && S == 32) {
+        my_pos = gpos ? __ldg(gpos + my_t) : my_t;
+        my_elig = !__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + my_pos);
+        dx = __ldcg(gdisp + 3 * (int64_t)my_t);
+        dy = __ldcg(gdisp + 3 * (int64_t)my_t + 1);
+        dz = __ldcg(gdisp + 3 * (int64_t)my_t + 2);
+      }
       if (tg < tgroups) {
 #pragma unroll 1
         for (int j = sub; j < n; j += S) {
@@ -554,32 +664,60 @@ struct SmemPath {
           const double wx = sh.wx[j], wy = sh.wy[j], wz = sh.wz[j];
 #pragma unroll
           for (int q = 0; q < kTPT; ++q)
-            pair_accum(px[q], py[q], pz[q], sx, sy, sz, wx, wy, wz, ax[q], ay[q], az[q]);
+            pair_accum(px[q], py[q], pz[q], sx, sy, sz, wx, wy, wz, v[4 * q], v[4 * q + 1], v[4 * q + 2]);
         }
       }
-#pragma unroll
-      for (int q = 0; q < kTPT; ++q) {
-        for (int off = S >> 1; off > 0; off >>= 1) {
-          ax[q] += __shfl_xor_sync(0xffffffffu, ax[q], off);
-          ay[q] += __shfl_xor_sync(0xffffffffu, ay[q], off);
-          az[q] += __shfl_xor_sync(0xffffffffu, az[q], off);
+      if (rd == 0) pc.mark(11);
+      if (S == 32) {
+        // one target group per warp: reduce-scatter, then lane q finishes target q
+        int idx;
+        const double tot = warp_reduce_scatter16(v, lane, idx);
+        const int w = tid >> 5;
+        if ((lane & 1) == 0 && (idx & 3) != 3) sh.acc[w][idx >> 2][idx & 3] = tot;
+        __syncwarp();
+        if (rd == 0) pc.mark(12);
+        if (mine) {
+          const double e = residual_norm(dx, dy, dz, sh.acc[w][lane][0], sh.acc[w][lane][1],
+                                         sh.acc[w][lane][2]);
+          s.err[my_t] = e;
+          bu = Best{e, my_pos};
+          if (my_elig) br = Best{e, my_pos};
         }
-      }
-      if (sub == 0) {
+        __syncwarp();
+      } else {
 #pragma unroll
         for (int q = 0; q < kTPT; ++q) {
-          if (pos[q] < 0) continue;
-          const int t = lo + kTPT * tg + q;
-          const double e = residual_norm(__ldcg(gdisp + 3 * (int64_t)t), __ldcg(gdisp + 3 * (int64_t)t + 1),
-                                         __ldcg(gdisp + 3 * (int64_t)t + 2), ax[q], ay[q], az[q]);
-          s.err[t] = e;
-          if (better(e, pos[q], bu.err, bu.pos)) bu = Best{e, pos[q]};
-          if (elig[q] && better(e, pos[q], br.err, br.pos)) br = Best{e, pos[q]};
+          for (int off = S >> 1; off > 0; off >>= 1) {
+            v[4 * q] += __shfl_xor_sync(0xffffffffu, v[4 * q], off);
+            v[4 * q + 1] += __shfl_xor_sync(0xffffffffu, v[4 * q + 1], off);
+            v[4 * q + 2] += __shfl_xor_sync(0xffffffffu, v[4 * q + 2], off);
+          }
+        }
+        if (rd == 0) pc.mark(12);
+        if (sub == 0 && tg < tgroups) {
+#pragma unroll
+          for (int q = 0; q < kTPT; ++q) {
+            const int t = lo + kTPT * tg + q;
+            if (t >= hi) continue;
+            const int pos = gpos ? __ldg(gpos + t) : t;
+            const double e = residual_norm(__ldcg(gdisp + 3 * (int64_t)t), __ldcg(gdisp + 3 * (int64_t)t + 1),
+                                           __ldcg(gdisp + 3 * (int64_t)t + 2), v[4 * q], v[4 * q + 1],
+                                           v[4 * q + 2]);
+            s.err[t] = e;
+            if (better(e, pos, bu.err, bu.pos)) bu = Best{e, pos};
+            if (!__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + pos) && better(e, pos, br.err, br.pos))
+              br = Best{e, pos};
+          }
         }
       }
+      if (rd == 0) pc.mark(13);
     }
-    publish(cta_best(sh.cm, bu, 0), 0, par);
-    publish(cta_best(sh.cm, br, 1), 1, par);
+    cta_best2(sh.cm, bu, br, S == 32 ? kTPT : 32);
+    if (tid < 32) {
+      publish(bu, 0, par);
+      publish(br, 1, par);
+    }
+    pc.mark(14);
   }
 
   __device__ int append(int pos, int& n, bool check_dup, double* pivot2_out) {
@@ -588,41 +726,72 @@ struct SmemPath {
     const int cap = a.cap;
     const double px = __ldg(a.points + 3 * (int64_t)pos), py = __ldg(a.points + 3 * (int64_t)pos + 1),
                  pz = __ldg(a.points + 3 * (int64_t)pos + 2);
-    const double dmin = exact_row(sh.cm, sh.row, n, px, py, pz, a.radius,
+    const bool near = exact_row(sh.cm, sh.row, n, px, py, pz, a.radius, a.dup_dist,
                                   [&](int j, double& x, double& y, double& z) {
                                     x = sh.ux[j];
                                     y = sh.uy[j];
                                     z = sh.uz[j];
                                   });
-    if (check_dup && n > 0 && dmin < a.dup_dist) return kRejectDup;
+    if (check_dup && n > 0 && near) return kRejectDup;
     pc.mark(1);
-    const int gw = rank * kLoopWarps + warp, nw = kClusterCTAs * kLoopWarps;
-    // c0 = Li row; each value stored into all 16 CTAs by lanes 0..15
-    for (int i = gw; i < n; i += nw) {
-      const double v = row_dot(a.Li + tri_off(i), i + 1, [&](int j) { return sh.row[j]; }, lane);
-      if (lane < kClusterCTAs) *at(&sh.c0[i], lane) = v;
-    }
+    // rows are dealt in pairs (p, n-1-p) so every warp carries about n+1
+    // elements; pair p lives on CTA p % 16, warp (p / 16) % 16
+    const int npairs = (n + 1) / 2;
+    auto for_my_pairs = [&](auto&& body) {
+      for (int p = rank + kClusterCTAs * warp; p < npairs; p += kClusterCTAs * kLoopWarps) {
+        const int ia = p, ib = n - 1 - p;
+        body(ia, ib == ia ? -1 : ib);
+      }
+    };
+    // c0 = Li row
+    for_my_pairs([&](int ia, int ib) {
+      double va, vb;
+      row_dot_pair(a.Li + tri_off(ia), ia + 1, a.Li + tri_off(ib < 0 ? 0 : ib), ib < 0 ? 0 : ib + 1,
+                   [&](int j) { return sh.row[j]; }, lane, va, vb);
+      if (lane < kClusterCTAs) {
+        *at(&sh.c0[ia], lane) = va;
+        if (ib >= 0) *at(&sh.c0[ib], lane) = vb;
+      }
+    });
     sync();
     pc.mark(2);
-    for (int i = gw; i < n; i += nw) {  // r = row - L c0
-      const double v = row_dot(a.L + tri_off(i), i + 1, [&](int j) { return sh.c0[j]; }, lane);
-      if (lane < kClusterCTAs) *at(&sh.r[i], lane) = sh.row[i] - v;
-    }
+    for_my_pairs([&](int ia, int ib) {  // r = row - L c0
+      double va, vb;
+      row_dot_pair(a.L + tri_off(ia), ia + 1, a.L + tri_off(ib < 0 ? 0 : ib), ib < 0 ? 0 : ib + 1,
+                   [&](int j) { return sh.c0[j]; }, lane, va, vb);
+      if (lane < kClusterCTAs) {
+        *at(&sh.r[ia], lane) = sh.row[ia] - va;
+        if (ib >= 0) *at(&sh.r[ib], lane) = sh.row[ib] - vb;
+      }
+    });
     sync();
     pc.mark(3);
     double pcc = 0.0, pcy0 = 0.0, pcy1 = 0.0, pcy2 = 0.0;
-    for (int i = gw; i < n; i += nw) {  // c = c0 + Li r
-      const double v = row_dot(a.Li + tri_off(i), i + 1, [&](int j) { return sh.r[j]; }, lane);
-      const double c = sh.c0[i] + v;
-      if (lane < kClusterCTAs) *at(&sh.c1[i], lane) = c;
+    for_my_pairs([&](int ia, int ib) {  // c = c0 + Li r
+      double va, vb;
+      row_dot_pair(a.Li + tri_off(ia), ia + 1, a.Li + tri_off(ib < 0 ? 0 : ib), ib < 0 ? 0 : ib + 1,
+                   [&](int j) { return sh.r[j]; }, lane, va, vb);
+      const double ca = sh.c0[ia] + va;
+      if (lane < kClusterCTAs) *at(&sh.c1[ia], lane) = ca;
       if (lane == 0) {
-        a.L[tri_off(n) + i] = c;  // row n of L (global)
-        pcc = fma(c, c, pcc);
-        pcy0 = fma(c, sh.y0[i], pcy0);
-        pcy1 = fma(c, sh.y1[i], pcy1);
-        pcy2 = fma(c, sh.y2[i], pcy2);
+        a.L[tri_off(n) + ia] = ca;  // row n of L (global)
+        pcc = fma(ca, ca, pcc);
+        pcy0 = fma(ca, sh.y0[ia], pcy0);
+        pcy1 = fma(ca, sh.y1[ia], pcy1);
+        pcy2 = fma(ca, sh.y2[ia], pcy2);
       }
-    }
+      if (ib >= 0) {
+        const double cb = sh.c0[ib] + vb;
+        if (lane < kClusterCTAs) *at(&sh.c1[ib], lane) = cb;
+        if (lane == 0) {
+          a.L[tri_off(n) + ib] = cb;
+          pcc = fma(cb, cb, pcc);
+          pcy0 = fma(cb, sh.y0[ib], pcy0);
+          pcy1 = fma(cb, sh.y1[ib], pcy1);
+          pcy2 = fma(cb, sh.y2[ib], pcy2);
+        }
+      }
+    });
     Common& cm = sh.cm;
     if (lane == 0) {
       cm.wred[warp][0] = pcc;
@@ -654,24 +823,78 @@ struct SmemPath {
     const double yn0 = (__ldg(a.disp + 3 * (int64_t)pos) - cm.dbl[2]) / l;
     const double yn1 = (__ldg(a.disp + 3 * (int64_t)pos + 1) - cm.dbl[3]) / l;
     const double yn2 = (__ldg(a.disp + 3 * (int64_t)pos + 2) - cm.dbl[4]) / l;
+    // column partials of u = Li^T c, v = Li^T y over this CTA's own rows:
+    // warp w owns 32-column chunks J = w, w + 16, ...; every load of a chunk
+    // is issued before its FMAs
+    const int nchunks = (n + 31) / 32;
+    for (int J = warp; J < nchunks; J += kLoopWarps) {
+      const int j = 32 * J + lane;
+      double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+      for (int p0 = rank; p0 < npairs; p0 += 8 * kClusterCTAs) {
+        double av[16];
+        int iv[16];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int p = p0 + u * kClusterCTAs;
+          const int ia = p < npairs ? p : -1;
+          const int ib = (p < npairs && n - 1 - p != p) ? n - 1 - p : -1;
+          iv[2 * u] = ia;
+          iv[2 * u + 1] = ib;
+          av[2 * u] = (ia >= 0 && j <= ia) ? __ldcg(a.Li + tri_off(ia) + j) : 0.0;
+          av[2 * u + 1] = (ib >= 0 && j <= ib) ? __ldcg(a.Li + tri_off(ib) + j) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int i = iv[u];
+          if (i >= 0 && j <= i) {
+            acc0 = fma(av[u], sh.c1[i], acc0);
+            acc1 = fma(av[u], sh.y0[i], acc1);
+            acc2 = fma(av[u], sh.y1[i], acc2);
+            acc3 = fma(av[u], sh.y2[i], acc3);
+          }
+        }
+      }
+      if (j < n) {
+        sh.colp[j][0] = acc0;
+        sh.colp[j][1] = acc1;
+        sh.colp[j][2] = acc2;
+        sh.colp[j][3] = acc3;
+      }
+    }
+    sync();
+    pc.mark(15);
+    // CTA `rank` folds columns [jlo, jhi) over the 16 CTAs in fixed order
+    const int per = (n + kClusterCTAs - 1) / kClusterCTAs;
+    const int jlo = rank * per, jhi = min(n, jlo + per);
+    for (int e = tid; e < (jhi - jlo) * 4; e += kLoopThreads) {
+      const int j = jlo + (e >> 2), c = e & 3;
+      double part[kClusterCTAs];
+#pragma unroll
+      for (int q = 0; q < kClusterCTAs; ++q) part[q] = *at(&sh.colp[j][c], q);
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < kClusterCTAs; ++q) t += part[q];
+      cm.red[e] = t;
+    }
+    __syncthreads();
     double* Lirow = a.Li + tri_off(n);
     double* wgt = a.sup + 3 * (int64_t)cap;
-    tri_cols<4, kLoopWarps>(
-        a.Li, n,
-        [&](int i, int c) { return c == 0 ? sh.c1[i] : (c == 1 ? sh.y0[i] : (c == 2 ? sh.y1[i] : sh.y2[i])); },
-        rank, kClusterCTAs, cm.red, [&](int j, const double* sum) {
-          const double lij = -sum[0] / l;
-          const double w0 = fma(lij, yn0, sum[1]), w1 = fma(lij, yn1, sum[2]), w2 = fma(lij, yn2, sum[3]);
-          Lirow[j] = lij;
-          wgt[j] = w0;
-          wgt[cap + j] = w1;
-          wgt[2 * cap + j] = w2;
-          for (int c = 0; c < kClusterCTAs; ++c) {
-            *at(&sh.wx[j], c) = w0;
-            *at(&sh.wy[j], c) = w1;
-            *at(&sh.wz[j], c) = w2;
-          }
-        });
+    for (int e = tid; e < (jhi - jlo) * kClusterCTAs; e += kLoopThreads) {
+      const int jj = e / kClusterCTAs, q = e % kClusterCTAs, j = jlo + jj;
+      const double lij = -cm.red[4 * jj] / l;
+      const double w0 = fma(lij, yn0, cm.red[4 * jj + 1]);
+      const double w1 = fma(lij, yn1, cm.red[4 * jj + 2]);
+      const double w2 = fma(lij, yn2, cm.red[4 * jj + 3]);
+      *at(&sh.wx[j], q) = w0;
+      *at(&sh.wy[j], q) = w1;
+      *at(&sh.wz[j], q) = w2;
+      if (q == 0) {
+        Lirow[j] = lij;
+        wgt[j] = w0;
+        wgt[cap + j] = w1;
+        wgt[2 * cap + j] = w2;
+      }
+    }
     if (tid == 0) {  // the new support, in every CTA's resident copy
       sh.ux[n] = px;
       sh.uy[n] = py;
@@ -703,6 +926,522 @@ struct SmemPath {
     }
     n += 1;
     sync();
+    pc.mark(5);
+    return kAccepted;
+  }
+};
+
+// ================================================================== MsgPath
+// 16-CTA cluster, everything a phase reads in shared memory, every
+// cross-CTA value pushed with st.async into the consumer's smem and counted
+// by the consumer's mbarrier (complete_tx). No cluster barrier and no
+// MEMBAR in steady state: a phase costs its math plus one DSMEM hop (~420
+// cycles measured, tools/barrier_bench.cu). Factor rows are owner-stable:
+// row i of L and Li lives in CTA i % 16 (packed), so the n < kMsgMax rows of
+// both factors fit next to the replicated vectors.
+constexpr int kMsgMax = 448;
+constexpr int kMsgOwnRows = kMsgMax / kClusterCTAs;                 // 28
+constexpr int kMsgOwnElems = 8 * kMsgOwnRows * (kMsgOwnRows - 1) + kMsgOwnRows * kClusterCTAs;
+constexpr int kMsgSlice = (kMsgMax + kClusterCTAs - 1) / kClusterCTAs;  // 28 columns
+constexpr int kMsgGoff = 512;   // group offsets cached in shared memory (else read from L2)
+
+enum MsgBar { kMbScan0 = 0, kMbScan1, kMbC0, kMbR, kMbC1, kMbColp, kMbW, kMbCount };
+
+struct MsgShared {
+  Common cm;
+  double ux[kMsgMax], uy[kMsgMax], uz[kMsgMax];  // support coordinates
+  double sx[kMsgMax], sy[kMsgMax], sz[kMsgMax];  // ... scaled by 1/R
+  double wx[kMsgMax], wy[kMsgMax], wz[kMsgMax];  // weights
+  double y0[kMsgMax], y1[kMsgMax], y2[kMsgMax];  // forward-substituted d
+  double row[kMsgMax], c0[kMsgMax], r[kMsgMax], c1[kMsgMax];
+  double Lown[kMsgOwnElems], Liown[kMsgOwnElems];  // owned rows i = 16 q + rank
+  double colp_in[kClusterCTAs][kMsgSlice][4];      // column partials for my slice
+  double rpart[kClusterCTAs][4];                   // c.c, c.y partials
+  double part_in[2][kClusterCTAs][2][2];           // scan partials (err, pos as double)
+  double acc[kLoopWarps][4][4];
+  int goff[kMsgGoff + 1];
+  alignas(8) unsigned long long mbar[kMbCount];
+};
+static_assert(sizeof(MsgShared) <= 227 * 1024, "MsgShared exceeds shared memory");
+static_assert(sizeof(SmemShared) <= 227 * 1024, "SmemShared exceeds shared memory");
+static_assert(sizeof(GlobalShared) <= 227 * 1024, "GlobalShared exceeds shared memory");
+
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ unsigned mapa(unsigned local, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async(unsigned raddr, double v, unsigned rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+               "d"(v), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async2(unsigned raddr, double v0, double v1, unsigned rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "d"(v0), "d"(v1), "r"(rbar)
+               : "memory");
+}
+
+struct MsgPath {
+  const rbf_gcb_args& a;
+  const LoopScratch& s;
+  MsgShared& sh;
+  double inv_r;
+  PhaseClock& pc;
+  unsigned phase_bits;  // parity of the next completion of each mbarrier
+
+  static constexpr int kMaxN = kMsgMax;
+  __device__ Common& cm() { return sh.cm; }
+  __device__ int rank() const { return blockIdx.x; }
+
+  __device__ static int own_off(int q, int rank) { return 8 * q * (q - 1) + q * (rank + 1); }
+
+  // -------------------------------------------------------------- mbarriers
+  __device__ void expect(int bar, unsigned bytes) {
+    if (threadIdx.x == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&sh.mbar[bar])),
+                   "r"(bytes)
+                   : "memory");
+  }
+  __device__ void wait(int bar) {
+    const unsigned parity = (phase_bits >> bar) & 1u;
+    const unsigned addr = smem_u32(&sh.mbar[bar]);
+    unsigned done = 0, spins = 0;
+    uint64_t t0 = 0;
+    while (true) {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(addr), "r"(parity)
+          : "memory");
+      if (done) break;
+      if ((++spins & 4095u) == 0) {
+        const uint64_t now = globaltimer_ns();
+        if (t0 == 0) {
+          t0 = now;
+        } else if (now - t0 > 20ull * 1000000000ull) {
+          atomicExch(s.fault, 2);
+          __trap();
+        }
+      }
+    }
+    phase_bits ^= 1u << bar;
+  }
+  // address of `p` (a field of MsgShared) in CTA `dst` and that CTA's mbarrier
+  __device__ __forceinline__ unsigned raddr(const void* p, int dst) { return mapa(smem_u32(p), dst); }
+  __device__ __forceinline__ unsigned rbar(int bar, int dst) { return mapa(smem_u32(&sh.mbar[bar]), dst); }
+
+  __device__ void sync() { cg::this_cluster().sync(); }
+
+  __device__ void begin(int n) {
+    const int cap = a.cap, rk = rank();
+    if (threadIdx.x == 0) {
+      for (int b = 0; b < kMbCount; ++b)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sh.mbar[b])) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    phase_bits = 0;
+    for (int j = threadIdx.x; j < n; j += kLoopThreads) {
+      const double x = __ldcg(a.sup + j), y = __ldcg(a.sup + cap + j), z = __ldcg(a.sup + 2 * cap + j);
+      sh.ux[j] = x;
+      sh.uy[j] = y;
+      sh.uz[j] = z;
+      sh.sx[j] = x * inv_r;
+      sh.sy[j] = y * inv_r;
+      sh.sz[j] = z * inv_r;
+      sh.wx[j] = __ldcg(a.sup + 3 * cap + j);
+      sh.wy[j] = __ldcg(a.sup + 4 * cap + j);
+      sh.wz[j] = __ldcg(a.sup + 5 * cap + j);
+      sh.y0[j] = __ldcg(a.y + 3 * j);
+      sh.y1[j] = __ldcg(a.y + 3 * j + 1);
+      sh.y2[j] = __ldcg(a.y + 3 * j + 2);
+    }
+    // owned factor rows i = 16 q + rank < n
+    for (int q = 0; 16 * q + rk < n; ++q) {
+      const int i = 16 * q + rk, o = own_off(q, rk);
+      for (int j = threadIdx.x; j <= i; j += kLoopThreads) {
+        sh.Lown[o + j] = __ldcg(a.L + tri_off(i) + j);
+        sh.Liown[o + j] = __ldcg(a.Li + tri_off(i) + j);
+      }
+    }
+    for (int g = threadIdx.x; g <= a.m && g <= kMsgGoff; g += kLoopThreads) sh.goff[g] = __ldg(a.group_off + g);
+    __syncthreads();
+  }
+  __device__ void finish() { sync(); }
+  __device__ int group_off(int g) { return a.m <= kMsgGoff ? sh.goff[g] : __ldg(a.group_off + g); }
+
+  // ---------------------------------------------------------------- partials
+  // lanes 0..15 of warp 0 hold the CTA's (bu, br): push them to every CTA
+  __device__ void publish2(Best bu, Best br, int par) {
+    if (threadIdx.x < kClusterCTAs) {
+      const int dst = threadIdx.x, bar = kMbScan0 + par;
+      st_async2(raddr(&sh.part_in[par][rank()][0][0], dst), bu.err, (double)bu.pos, rbar(bar, dst));
+      st_async2(raddr(&sh.part_in[par][rank()][1][0], dst), br.err, (double)br.pos, rbar(bar, dst));
+    }
+  }
+  __device__ void publish(Best b, int slot, int par) {  // seeds: slot 0 only
+    publish2(b, Best{-1.0, kNone}, par);
+  }
+  // wait for the 16 CTAs' partials of this parity and fold them (fixed order)
+  __device__ void gather(int par, int nslots) {
+    expect(kMbScan0 + par, kClusterCTAs * 32);
+    wait(kMbScan0 + par);
+    if (threadIdx.x < 32 * nslots) {
+      const int slot = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      Best b{-1.0, kNone};
+      if (lane < kClusterCTAs)
+        b = Best{sh.part_in[par][lane][slot][0], (int)sh.part_in[par][lane][slot][1]};
+      b = warp_best(b);
+      if (lane == 0) sh.cm.bcast[slot] = b;
+    }
+    __syncthreads();
+  }
+
+  // -------------------------------------------------------------------- scan
+  // targets per lane chosen so the CTA's rows fill as many warps as possible
+  __device__ void scan(const int* gpos, const double* gpt, const double* gdisp, int card, int n,
+                       int par) {
+    const int lo = (int)((int64_t)card * blockIdx.x / kClusterCTAs);
+    const int hi = (int)((int64_t)card * (blockIdx.x + 1) / kClusterCTAs);
+    const int mine = hi - lo;
+    if (mine <= kLoopWarps)
+      scan_t<1>(gpos, gpt, gdisp, lo, hi, n, par);
+    else if (mine <= 2 * kLoopWarps)
+      scan_t<2>(gpos, gpt, gdisp, lo, hi, n, par);
+    else if (mine <= 3 * kLoopWarps)
+      scan_t<3>(gpos, gpt, gdisp, lo, hi, n, par);
+    else
+      scan_t<4>(gpos, gpt, gdisp, lo, hi, n, par);
+  }
+
+  template <int kTPT>
+  __device__ void scan_t(const int* gpos, const double* gpt, const double* gdisp, int lo, int hi, int n,
+                         int par) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int tgroups = (hi - lo + kTPT - 1) / kTPT;
+    int S = 32;
+    while (S > 1 && tgroups * S > kLoopThreads) S >>= 1;
+    const int per_round = kLoopThreads / S;
+    const int rounds = (tgroups + per_round - 1) / per_round;
+    const int sub = tid % S;
+    Best bu{-1.0, kNone}, br{-1.0, kNone};
+    for (int rd = 0; rd < rounds; ++rd) {
+      const int tg = rd * per_round + tid / S;
+      double px[kTPT], py[kTPT], pz[kTPT];
+      double v[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = 0.0;
+#pragma unroll
+      for (int q = 0; q < kTPT; ++q) {
+        const int t = lo + kTPT * tg + q;
+        const bool ok = tg < tgroups && t < hi;
+        px[q] = ok ? __ldcg(gpt + 3 * (int64_t)t) * inv_r : 0.0;
+        py[q] = ok ? __ldcg(gpt + 3 * (int64_t)t + 1) * inv_r : 0.0;
+        pz[q] = ok ? __ldcg(gpt + 3 * (int64_t)t + 2) * inv_r : 0.0;
+        v[4 * q] = v[4 * q + 1] = v[4 * q + 2] = v[4 * q + 3] = 0.0;
+      }
+      const int my_t = lo + kTPT * tg + (S == 32 ? lane : 0);
+      const bool mine = S == 32 && lane < kTPT && tg < tgroups && my_t < hi;
+      int my_pos = -1;
+      bool my_elig = false;
+      double dx = 0.0, dy = 0.0, dz = 0.0;
+      if (mine) {
+        my_pos = gpos ? __ldg(gpos + my_t) : my_t;
+        my_elig = !__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + my_pos);
+        dx = __ldcg(gdisp + 3 * (int64_t)my_t);
+        dy = __ldcg(gdisp + 3 * (int64_t)my_t + 1);
+        dz = __ldcg(gdisp + 3 * (int64_t)my_t + 2);
+      }
+      if (tg < tgroups) {
+#pragma unroll 1
+        for (int j = sub; j < n; j += S) {
+          const double sx = sh.sx[j], sy = sh.sy[j], sz = sh.sz[j];
+          const double wx = sh.wx[j], wy = sh.wy[j], wz = sh.wz[j];
+#pragma unroll
+          for (int q = 0; q < kTPT; ++q)
+            pair_accum(px[q], py[q], pz[q], sx, sy, sz, wx, wy, wz, v[4 * q], v[4 * q + 1], v[4 * q + 2]);
+        }
+      }
+      if (rd == 0) pc.mark(11);
+      if (S == 32) {
+        int idx;
+        const double tot = warp_reduce_scatter16(v, lane, idx);
+        const int w = tid >> 5;
+        if ((lane & 1) == 0 && (idx & 3) != 3) sh.acc[w][idx >> 2][idx & 3] = tot;
+        __syncwarp();
+        if (rd == 0) pc.mark(12);
+        if (mine) {
+          const double e = residual_norm(dx, dy, dz, sh.acc[w][lane][0], sh.acc[w][lane][1],
+                                         sh.acc[w][lane][2]);
+          s.err[my_t] = e;
+          bu = Best{e, my_pos};
+          if (my_elig) br = Best{e, my_pos};
+        }
+        __syncwarp();
+      } else {
+#pragma unroll
+        for (int q = 0; q < kTPT; ++q) {
+          for (int off = S >> 1; off > 0; off >>= 1) {
+            v[4 * q] += __shfl_xor_sync(0xffffffffu, v[4 * q], off);
+            v[4 * q + 1] += __shfl_xor_sync(0xffffffffu, v[4 * q + 1], off);
+            v[4 * q + 2] += __shfl_xor_sync(0xffffffffu, v[4 * q + 2], off);
+          }
+        }
+        if (rd == 0) pc.mark(12);
+        if (sub == 0 && tg < tgroups) {
+#pragma unroll
+          for (int q = 0; q < kTPT; ++q) {
+            const int t = lo + kTPT * tg + q;
+            if (t >= hi) continue;
+            const int pos = gpos ? __ldg(gpos + t) : t;
+            const double e = residual_norm(__ldcg(gdisp + 3 * (int64_t)t), __ldcg(gdisp + 3 * (int64_t)t + 1),
+                                           __ldcg(gdisp + 3 * (int64_t)t + 2), v[4 * q], v[4 * q + 1],
+                                           v[4 * q + 2]);
+            s.err[t] = e;
+            if (better(e, pos, bu.err, bu.pos)) bu = Best{e, pos};
+            if (!__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + pos) && better(e, pos, br.err, br.pos))
+              br = Best{e, pos};
+          }
+        }
+      }
+      if (rd == 0) pc.mark(13);
+    }
+    cta_best2(sh.cm, bu, br, S == 32 ? kTPT : 32);
+    if (threadIdx.x < 32) publish2(bu, br, par);
+    pc.mark(14);
+  }
+
+  // ------------------------------------------------------------------ append
+  // owned rows: q = 0.. with i = 16 q + rank < n; warp w takes q = w, w + 16
+  template <typename F>
+  __device__ __forceinline__ void for_owned_rows(int n, F&& body) {
+    const int warp = threadIdx.x >> 5;
+    for (int q = warp; 16 * q + rank() < n; q += kLoopWarps) body(q, 16 * q + rank());
+  }
+
+  template <typename XL>
+  __device__ __forceinline__ double own_dot(const double* M, int q, int i, XL x, int lane) {
+    const double* rowp = M + own_off(q, rank());
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int j0 = 0; j0 <= i; j0 += 8 * kWarp) {
+      double av[8], xv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + u * kWarp + lane;
+        av[u] = j <= i ? rowp[j] : 0.0;
+        xv[u] = j <= i ? x(j) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) {
+        acc0 = fma(av[u], xv[u], acc0);
+        acc1 = fma(av[u + 1], xv[u + 1], acc1);
+      }
+    }
+    return warp_sum(acc0 + acc1);
+  }
+
+  // value v of owned row i -> vector `vec` in all 16 CTAs (lanes 0..15 send)
+  __device__ __forceinline__ void bcast(double* vec, int i, double v, int bar, int lane) {
+    if (lane < kClusterCTAs) st_async(raddr(&vec[i], lane), v, rbar(bar, lane));
+  }
+
+  __device__ int append(int pos, int& n, bool check_dup, double* pivot2_out) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rk = rank();
+    const int cap = a.cap;
+    const double px = __ldg(a.points + 3 * (int64_t)pos), py = __ldg(a.points + 3 * (int64_t)pos + 1),
+                 pz = __ldg(a.points + 3 * (int64_t)pos + 2);
+    const bool near = exact_row(sh.cm, sh.row, n, px, py, pz, a.radius, a.dup_dist,
+                                  [&](int j, double& x, double& y, double& z) {
+                                    x = sh.ux[j];
+                                    y = sh.uy[j];
+                                    z = sh.uz[j];
+                                  });
+    if (check_dup && n > 0 && near) return kRejectDup;
+    pc.mark(1);
+    // c0 = Li row
+    expect(kMbC0, n * 8);
+    for_owned_rows(n, [&](int q, int i) {
+      bcast(sh.c0, i, own_dot(sh.Liown, q, i, [&](int j) { return sh.row[j]; }, lane), kMbC0, lane);
+    });
+    wait(kMbC0);
+    pc.mark(2);
+    // r = row - L c0
+    expect(kMbR, n * 8);
+    for_owned_rows(n, [&](int q, int i) {
+      bcast(sh.r, i, sh.row[i] - own_dot(sh.Lown, q, i, [&](int j) { return sh.c0[j]; }, lane), kMbR, lane);
+    });
+    wait(kMbR);
+    pc.mark(3);
+    // c = c0 + Li r, partial sums of c.c and c.y over the owned rows
+    expect(kMbC1, n * 8 + kClusterCTAs * 32);
+    double pcc = 0.0, pcy0 = 0.0, pcy1 = 0.0, pcy2 = 0.0;
+    for_owned_rows(n, [&](int q, int i) {
+      const double c = sh.c0[i] + own_dot(sh.Liown, q, i, [&](int j) { return sh.r[j]; }, lane);
+      bcast(sh.c1, i, c, kMbC1, lane);
+      pcc = fma(c, c, pcc);
+      pcy0 = fma(c, sh.y0[i], pcy0);
+      pcy1 = fma(c, sh.y1[i], pcy1);
+      pcy2 = fma(c, sh.y2[i], pcy2);
+    });
+    Common& cm = sh.cm;
+    if (lane == 0) {
+      cm.wred[warp][0] = pcc;
+      cm.wred[warp][1] = pcy0;
+      cm.wred[warp][2] = pcy1;
+      cm.wred[warp][3] = pcy2;
+    }
+    __syncthreads();
+    if (tid < 4 * kClusterCTAs) {  // CTA partial (warp order) -> every CTA
+      const int c = tid & 3, dst = tid >> 2;
+      double t = 0.0;
+      for (int w = 0; w < kLoopWarps; ++w) t += cm.wred[w][c];
+      st_async(raddr(&sh.rpart[rk][c], dst), t, rbar(kMbC1, dst));
+    }
+    wait(kMbC1);
+    pc.mark(4);
+    if (tid < 4) {  // fixed-order fold of the 16 CTA partials
+      double t = 0.0;
+      for (int c = 0; c < kClusterCTAs; ++c) t += sh.rpart[c][tid];
+      cm.dbl[1 + tid] = t;
+    }
+    __syncthreads();
+    const double pivot2 = 1.0 - cm.dbl[1];  // row[n] = phi(0) = 1 exactly
+    *pivot2_out = pivot2;
+    if (!(pivot2 > 0.0)) {
+      __syncthreads();
+      return kRejectPivot;
+    }
+    const double l = sqrt(pivot2);
+    const double yn0 = (__ldg(a.disp + 3 * (int64_t)pos) - cm.dbl[2]) / l;
+    const double yn1 = (__ldg(a.disp + 3 * (int64_t)pos + 1) - cm.dbl[3]) / l;
+    const double yn2 = (__ldg(a.disp + 3 * (int64_t)pos + 2) - cm.dbl[4]) / l;
+    // column partials of u = Li^T c, v = Li^T y over the owned rows, pushed
+    // to the CTA that owns the column slice
+    const int per = (n + kClusterCTAs - 1) / kClusterCTAs;
+    const int jlo = rk * per, jhi = min(n, jlo + per);
+    expect(kMbColp, (unsigned)(kClusterCTAs * max(jhi - jlo, 0) * 32));
+    const int nchunks = (n + 31) / 32;
+    const int nown = n > rk ? (n - rk + kClusterCTAs - 1) / kClusterCTAs : 0;
+    for (int J = warp; J < nchunks; J += kLoopWarps) {
+      const int j = 32 * J + lane;
+      double u = 0.0, v0 = 0.0, v1 = 0.0, v2 = 0.0;
+      // rows i = 16 q + rk >= j only: start at the first such q
+      const int q0 = j > rk ? (j - rk + kClusterCTAs - 1) / kClusterCTAs : 0;
+      for (int qb = q0; qb < nown; qb += 4) {
+        double lv[4], cv[4], y0v[4], y1v[4], y2v[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int q = qb + t, i = 16 * q + rk;
+          const bool ok = q < nown && j <= i;
+          lv[t] = ok ? sh.Liown[own_off(q, rk) + j] : 0.0;
+          cv[t] = ok ? sh.c1[i] : 0.0;
+          y0v[t] = ok ? sh.y0[i] : 0.0;
+          y1v[t] = ok ? sh.y1[i] : 0.0;
+          y2v[t] = ok ? sh.y2[i] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          u = fma(lv[t], cv[t], u);
+          v0 = fma(lv[t], y0v[t], v0);
+          v1 = fma(lv[t], y1v[t], v1);
+          v2 = fma(lv[t], y2v[t], v2);
+        }
+      }
+      if (j < n) {
+        const int dst = j / per;
+        const unsigned b = rbar(kMbColp, dst);
+        const unsigned p0 = raddr(&sh.colp_in[rk][j - dst * per][0], dst);
+        st_async2(p0, u, v0, b);
+        st_async2(p0 + 16, v1, v2, b);
+      }
+    }
+    wait(kMbColp);
+    pc.mark(15);
+    // my column slice: fold the 16 partials (fixed order), new Li row n
+    // entries to its owner, new weights to every CTA
+    const int owner = n % kClusterCTAs, qn = n / kClusterCTAs;
+    expect(kMbW, (unsigned)(n * 24 + (owner == rk ? n * 8 : 0)));
+    double* Lirow_g = a.Li + tri_off(n);
+    double* wgt = a.sup + 3 * (int64_t)cap;
+    for (int e = tid; e < (jhi - jlo) * 4; e += kLoopThreads) {  // fixed-order fold
+      const int jj = e >> 2, c = e & 3;
+      double part[kClusterCTAs];
+#pragma unroll
+      for (int q = 0; q < kClusterCTAs; ++q) part[q] = sh.colp_in[q][jj][c];
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < kClusterCTAs; ++q) t += part[q];
+      cm.red[e] = t;
+    }
+    __syncthreads();
+    for (int e = tid; e < (jhi - jlo) * kClusterCTAs; e += kLoopThreads) {
+      const int jj = e / kClusterCTAs, dst = e % kClusterCTAs, j = jlo + jj;
+      const double lij = -cm.red[4 * jj] / l;
+      const double w0 = fma(lij, yn0, cm.red[4 * jj + 1]), w1 = fma(lij, yn1, cm.red[4 * jj + 2]),
+                   w2 = fma(lij, yn2, cm.red[4 * jj + 3]);
+      const unsigned b = rbar(kMbW, dst);
+      st_async(raddr(&sh.wx[j], dst), w0, b);
+      st_async(raddr(&sh.wy[j], dst), w1, b);
+      st_async(raddr(&sh.wz[j], dst), w2, b);
+      if (dst == owner) st_async(raddr(&sh.Liown[own_off(qn, owner) + j], dst), lij, b);
+      if (dst == 0) {
+        Lirow_g[j] = lij;
+        wgt[j] = w0;
+        wgt[cap + j] = w1;
+        wgt[2 * cap + j] = w2;
+      }
+    }
+    // the new support, in every CTA's resident copy
+    if (tid == 0) {
+      sh.ux[n] = px;
+      sh.uy[n] = py;
+      sh.uz[n] = pz;
+      sh.sx[n] = px * inv_r;
+      sh.sy[n] = py * inv_r;
+      sh.sz[n] = pz * inv_r;
+      sh.y0[n] = yn0;
+      sh.y1[n] = yn1;
+      sh.y2[n] = yn2;
+      a.inel[pos] = 1;
+      if (rk == 0) {  // global copies
+        a.y[3 * (int64_t)n] = yn0;
+        a.y[3 * (int64_t)n + 1] = yn1;
+        a.y[3 * (int64_t)n + 2] = yn2;
+        a.sup[n] = px;
+        a.sup[cap + n] = py;
+        a.sup[2 * cap + n] = pz;
+        wgt[n] = yn0 / l;
+        wgt[cap + n] = yn1 / l;
+        wgt[2 * cap + n] = yn2 / l;
+        a.sel[n] = pos;
+        Lirow_g[n] = 1.0 / l;
+        a.L[tri_off(n) + n] = l;
+      }
+    }
+    if (rk == owner) {  // row n of L = [c, l] (c replicated), diagonal of Li
+      const int o = own_off(qn, owner);
+      for (int j = tid; j < n; j += kLoopThreads) {
+        sh.Lown[o + j] = sh.c1[j];
+        a.L[tri_off(n) + j] = sh.c1[j];
+      }
+      if (tid == 0) {
+        sh.Lown[o + n] = l;
+        sh.Liown[o + n] = 1.0 / l;
+      }
+    }
+    wait(kMbW);
+    if (tid == 0) {
+      sh.wx[n] = yn0 / l;
+      sh.wy[n] = yn1 / l;
+      sh.wz[n] = yn2 / l;
+    }
+    n += 1;
+    __syncthreads();
     pc.mark(5);
     return kAccepted;
   }
@@ -755,8 +1494,7 @@ __device__ void device_seeds(Path& P, const rbf_gcb_args& a, const LoopScratch& 
     if (better(m, i, b.err, b.pos)) b = Best{m, i};
   }
   P.publish(cta_best(P.cm(), b, 0), 0, par);
-  P.sync();
-  P.fold(par, 1);
+  P.gather(par, 1);
   par ^= 1;
   seeds[0] = P.cm().bcast[0].pos;
   for (int q = 1; q < 3; ++q) {
@@ -773,8 +1511,7 @@ __device__ void device_seeds(Path& P, const rbf_gcb_args& a, const LoopScratch& 
     }
     __syncthreads();
     P.publish(cta_best(P.cm(), bb, 0), 0, par);
-    P.sync();
-    P.fold(par, 1);
+    P.gather(par, 1);
     par ^= 1;
     seeds[q] = P.cm().bcast[0].pos;
   }
@@ -800,7 +1537,7 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
 
   auto save = [&](int status, int want_mode) {
     if (leader) {
-      for (int i = 0; i < 12; ++i) st->phase_cycles[i] += cm.phase[i];
+      for (int i = 0; i < 16; ++i) st->phase_cycles[i] += cm.phase[i];
       st->n = n;
       st->k = k;
       st->streak_ok = streak_ok;
@@ -850,7 +1587,8 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
       break;
     }
     if (n >= Path::kMaxN - 1) {  // beyond this path's resident capacity
-      save(RBF_EGROW, self_mode == RBF_GCB_SMEM ? RBF_GCB_CLUSTER : self_mode);
+      save(RBF_EGROW, self_mode == RBF_GCB_MSG ? RBF_GCB_SMEM
+                      : self_mode == RBF_GCB_SMEM ? RBF_GCB_CLUSTER : self_mode);
       return;
     }
     if (n >= a.cap || nrec >= a.rec_cap) {
@@ -859,15 +1597,14 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
     }
     const uint64_t t_a = leader_timer();
     const int gi = k % m;
-    const int off = __ldg(a.group_off + gi);
-    const int card = __ldg(a.group_off + gi + 1) - off;
+    const int off = P.group_off(gi);
+    const int card = P.group_off(gi + 1) - off;
     const int* gpos = a.group_pos + off;
     pc.mark(6);
     P.scan(gpos, s.gpt + 3 * (int64_t)off, s.gdisp + 3 * (int64_t)off, card, n, par);
-    P.sync();
+    P.gather(par, 2);
     pc.mark(0);
     pc.count(10);
-    P.fold(par, 2);
     par ^= 1;
     const Best bu = cm.bcast[0];
     Best cand = cm.bcast[1];
@@ -890,7 +1627,7 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
           a.inel[cand.pos] = 1;
           __threadfence();
         }
-        __syncthreads();
+        P.sync();  // rare path: every CTA's errors (global) visible
         cand = rescan_candidate(a, s, cm, gpos, card);
       }
     }
@@ -934,8 +1671,7 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
   const uint64_t t_a = leader_timer();
   pc.mark(6);
   P.scan(nullptr, a.points, a.disp, a.nb, n, par);
-  P.sync();
-  P.fold(par, 1);
+  P.gather(par, 1);
   par ^= 1;
   pc.mark(8);
   const Best bu = cm.bcast[0];
@@ -982,12 +1718,22 @@ __global__ void __launch_bounds__(kLoopThreads, 1) gcb_smem_kernel(rbf_gcb_args 
   pc.start(sh.cm.phase);
   SmemPath P{a, s, sh, 1.0 / a.radius, pc};
   gcb_driver(P, a, s, pc, RBF_GCB_SMEM);
+  P.finish();
+}
+
+__global__ void __launch_bounds__(kLoopThreads, 1) gcb_msg_kernel(rbf_gcb_args a, LoopScratch s) {
+  MsgShared& sh = *reinterpret_cast<MsgShared*>(g_smem);
+  PhaseClock pc;
+  pc.start(sh.cm.phase);
+  MsgPath P{a, s, sh, 1.0 / a.radius, pc, 0u};
+  gcb_driver(P, a, s, pc, RBF_GCB_MSG);
+  P.finish();
 }
 
 static int resolve_mode(int mode, int nb, int m) {
   if (mode != RBF_GCB_AUTO) return mode;
   const int card = (nb + m - 1) / m;
-  return card <= kAutoClusterMaxCard ? RBF_GCB_SMEM : RBF_GCB_GRID;
+  return card <= kAutoClusterMaxCard ? RBF_GCB_MSG : RBF_GCB_GRID;
 }
 
 static cudaError_t launch_cluster(const void* fn, rbf_gcb_args& a, LoopScratch& s, size_t smem,
@@ -1027,7 +1773,7 @@ extern "C" int rbf_device_info(int device, int* sm_count_host, int* loop_ctas_ho
 extern "C" int rbf_gcb_ctas(int32_t mode, int32_t nb, int32_t m, int32_t* ctas_host,
                             int32_t* resolved_mode_host) {
   if (nb < 1 || m < 1) return set_error(RBF_EARG, "bad nb/m");
-  if (mode < RBF_GCB_AUTO || mode > RBF_GCB_SMEM) return set_error(RBF_EARG, "bad mode %d", mode);
+  if (mode < RBF_GCB_AUTO || mode > RBF_GCB_MSG) return set_error(RBF_EARG, "bad mode %d", mode);
   int dev = 0;
   RBF_CUDA_TRY(cudaGetDevice(&dev));
   const int r = resolve_mode(mode, nb, m);
@@ -1063,7 +1809,9 @@ extern "C" int rbf_gcb_run(const rbf_gcb_args* args, void* stream) {
   cudaStream_t st = as_stream(stream);
   RBF_CUDA_TRY(cudaMemsetAsync(s.bar, 0, 64, st));
   rbf_gcb_args acopy = a;
-  if (mode == RBF_GCB_SMEM) {
+  if (mode == RBF_GCB_MSG) {
+    RBF_CUDA_TRY(launch_cluster((const void*)gcb_msg_kernel, acopy, s, sizeof(MsgShared), st));
+  } else if (mode == RBF_GCB_SMEM) {
     RBF_CUDA_TRY(launch_cluster((const void*)gcb_smem_kernel, acopy, s, sizeof(SmemShared), st));
   } else if (mode == RBF_GCB_CLUSTER) {
     RBF_CUDA_TRY(launch_cluster((const void*)gcb_cluster_kernel, acopy, s, sizeof(GlobalShared), st));

@@ -385,7 +385,7 @@ def test_selection_cluster_and_grid_modes(cuda, name):
     radius, tol, cap, m, seed = g["params"]
     b = cuda.BoundarySet(np.arange(len(pts)), pts, disp)
     cfg = cuda.SelectionConfig(radius=radius, tol=tol, max_supports=int(cap), m=int(m), seed=int(seed))
-    for mode in (N.GCB_SMEM, N.GCB_CLUSTER, N.GCB_GRID):
+    for mode in (N.GCB_MSG, N.GCB_SMEM, N.GCB_CLUSTER, N.GCB_GRID):
         res = _gcb_run(b, cfg, mode=mode)
         assert np.array_equal(res.support.nodes, g["seq"]), mode
         assert [r.node for r in res.history.records] == g["rec_node"].tolist()
