@@ -286,6 +286,53 @@ def eval_device(points, support_points, weights, radius, deform=False, out=None)
     return out
 
 
+_PIPELINE_MIN = 1 << 18   # host inputs at least this long are streamed in chunks
+_PIPELINE_CHUNKS = 8
+_streams = {}
+
+
+def _pipeline_streams():
+    t = N.torch()
+    dev = t.cuda.current_device()
+    if dev not in _streams:
+        _streams[dev] = (t.cuda.Stream(), t.cuda.Stream())
+    return _streams[dev]
+
+
+def _eval_host_pipelined(points, s, w, radius, deform):
+    """Host (n, 3) points -> host result, the n targets streamed in chunks so
+    the host->device copy of chunk k+1 and the device->host copy of chunk
+    k-1 overlap the kernel on chunk k (PCIe is full duplex). Per-target
+    results are bitwise those of one launch."""
+    t = N.torch()
+    n = len(points)
+    src = t.from_numpy(points)  # pinned memory streams asynchronously; pageable copies block per chunk
+    dev_in = t.empty((n, 3), dtype=t.float64, device=_device())
+    dev_out = t.empty((n, 3), dtype=t.float64, device=_device())
+    host_out = t.empty((n, 3), dtype=t.float64, pin_memory=True)
+    copy_in, copy_out = _pipeline_streams()
+    compute = t.cuda.current_stream()
+    step = -(-n // _PIPELINE_CHUNKS)
+    step = -(-step // 512) * 512
+    for lo in range(0, n, step):
+        hi = min(n, lo + step)
+        with t.cuda.stream(copy_in):
+            dev_in[lo:hi].copy_(src[lo:hi], non_blocking=True)
+            ready = t.cuda.Event()
+            ready.record(copy_in)
+        compute.wait_event(ready)
+        eval_device(dev_in[lo:hi], s, w, radius, deform=deform, out=dev_out[lo:hi])
+        done = t.cuda.Event()
+        done.record(compute)
+        copy_out.wait_event(done)
+        with t.cuda.stream(copy_out):
+            host_out[lo:hi].copy_(dev_out[lo:hi], non_blocking=True)
+    copy_out.synchronize()
+    # keep the device buffers alive until the copies that use them are done
+    compute.wait_stream(copy_out)
+    return host_out.numpy()
+
+
 def _eval_displacements(points, support_points, weights, radius, workers=1, deform=False):
     """sum_i w_i phi(|p - s_i| / R) at every point (reference core.py:301-334)."""
     t = N.torch()
@@ -294,9 +341,11 @@ def _eval_displacements(points, support_points, weights, radius, workers=1, defo
     n = len(points)
     if n == 0:
         return t.zeros((0, 3), dtype=t.float64) if as_torch else np.zeros((0, 3))
-    p = _to_device(points)
     s = _to_device(support_points)
     w = _to_device(weights)
+    if not as_torch and n >= _PIPELINE_MIN:
+        return _eval_host_pipelined(np.ascontiguousarray(points, dtype=np.float64), s, w, radius, deform)
+    p = _to_device(points)
     out = eval_device(p, s, w, radius, deform=deform)
     return out if as_torch else _to_host(out)
 

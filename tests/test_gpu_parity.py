@@ -107,6 +107,23 @@ def test_eval_shards_are_bitwise_identical(cuda, rng):
     assert np.array_equal(cuda.evaluate_displacements(q, s, 2.0, workers=8), full)
 
 
+def test_eval_pipelined_host_path_bitwise(cuda, rng):
+    """Host inputs above the streaming threshold go through the chunked
+    H2D / kernel / D2H pipeline: same bits as one device launch."""
+    import torch
+
+    pts = rng.normal(size=(90, 3))
+    s = cuda.SupportSet(np.arange(90), pts, rng.normal(size=(90, 3)))
+    q = rng.normal(size=(300_001, 3))
+    host = cuda.deform_points(q, s, 2.0)
+    pinned = torch.from_numpy(q).pin_memory().numpy()
+    host_pinned = cuda.deform_points(pinned, s, 2.0)
+    dev = cuda.deform_points(torch.from_numpy(q).cuda(), s, 2.0).cpu().numpy()
+    assert np.array_equal(host, dev) and np.array_equal(host_pinned, dev)
+    assert np.array_equal(cuda.evaluate_displacements(q, s, 2.0),
+                          cuda.evaluate_displacements(torch.from_numpy(q).cuda(), s, 2.0).cpu().numpy())
+
+
 def test_eval_torch_device_path(cuda, rng):
     import torch
 
