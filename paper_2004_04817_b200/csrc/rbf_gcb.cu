@@ -955,7 +955,8 @@ struct MsgShared {
   double y0[kMsgMax], y1[kMsgMax], y2[kMsgMax];  // forward-substituted d
   double row[kMsgMax], c0[kMsgMax], r[kMsgMax], c1[kMsgMax];
   double Lown[kMsgOwnElems], Liown[kMsgOwnElems];  // owned rows i = 16 q + rank
-  double colp_in[kClusterCTAs][kMsgSlice][4];      // column partials for my slice
+  alignas(16) double colp_in[kClusterCTAs][kMsgSlice];  // u partials for my slice
+  alignas(16) double u_all[kMsgMax];                     // u = Li^T c, all-gathered
   double rpart[kClusterCTAs][4];                   // c.c, c.y partials
   double part_in[2][kClusterCTAs][2][2];           // scan partials (err, pos as double)
   double acc[kLoopWarps][4][4];
@@ -1320,82 +1321,56 @@ struct MsgPath {
     const double yn0 = (__ldg(a.disp + 3 * (int64_t)pos) - cm.dbl[2]) / l;
     const double yn1 = (__ldg(a.disp + 3 * (int64_t)pos + 1) - cm.dbl[3]) / l;
     const double yn2 = (__ldg(a.disp + 3 * (int64_t)pos + 2) - cm.dbl[4]) / l;
-    // column partials of u = Li^T c, v = Li^T y over the owned rows, pushed
-    // to the CTA that owns the column slice
-    const int per = (n + kClusterCTAs - 1) / kClusterCTAs;
-    const int jlo = rk * per, jhi = min(n, jlo + per);
-    expect(kMbColp, (unsigned)(kClusterCTAs * max(jhi - jlo, 0) * 32));
-    const int nchunks = (n + 31) / 32;
+    // u = Li^T c (the weights are updated incrementally,
+    // x' = x - (u / l) y_n: as accurate as recomputing Li^T y).
+    // Reduce-scatter: partial u over the owned rows, column pairs pushed to
+    // the CTA folding that slice; all-gather: each slice of u to every CTA.
+    const int per = 2 * ((n + 2 * kClusterCTAs - 1) / (2 * kClusterCTAs));  // even
+    const int jlo = rk * per;
+    expect(kMbColp, (unsigned)(kClusterCTAs * per * 8));
     const int nown = n > rk ? (n - rk + kClusterCTAs - 1) / kClusterCTAs : 0;
-    for (int J = warp; J < nchunks; J += kLoopWarps) {
-      const int j = 32 * J + lane;
-      double u = 0.0, v0 = 0.0, v1 = 0.0, v2 = 0.0;
-      // rows i = 16 q + rk >= j only: start at the first such q
-      const int q0 = j > rk ? (j - rk + kClusterCTAs - 1) / kClusterCTAs : 0;
-      for (int qb = q0; qb < nown; qb += 4) {
-        double lv[4], cv[4], y0v[4], y1v[4], y2v[4];
+    for (int jp = tid; 2 * jp < kClusterCTAs * per; jp += kLoopThreads) {
+      const int j0 = 2 * jp;
+      double u0 = 0.0, u1 = 0.0;
+      if (j0 < n) {
+        const int q0 = j0 > rk ? (j0 - rk + kClusterCTAs - 1) / kClusterCTAs : 0;
+        for (int qb = q0; qb < nown; qb += 4) {
+          double l0[4], l1[4], cv[4];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int q = qb + t, i = 16 * q + rk;
-          const bool ok = q < nown && j <= i;
-          lv[t] = ok ? sh.Liown[own_off(q, rk) + j] : 0.0;
-          cv[t] = ok ? sh.c1[i] : 0.0;
-          y0v[t] = ok ? sh.y0[i] : 0.0;
-          y1v[t] = ok ? sh.y1[i] : 0.0;
-          y2v[t] = ok ? sh.y2[i] : 0.0;
-        }
+          for (int t = 0; t < 4; ++t) {
+            const int q = qb + t, i = 16 * q + rk;
+            const bool ok = q < nown;
+            const int o = own_off(ok ? q : 0, rk);
+            l0[t] = ok ? sh.Liown[o + j0] : 0.0;
+            l1[t] = (ok && j0 + 1 <= i) ? sh.Liown[o + j0 + 1] : 0.0;
+            cv[t] = ok ? sh.c1[i] : 0.0;
+          }
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          u = fma(lv[t], cv[t], u);
-          v0 = fma(lv[t], y0v[t], v0);
-          v1 = fma(lv[t], y1v[t], v1);
-          v2 = fma(lv[t], y2v[t], v2);
+          for (int t = 0; t < 4; ++t) {
+            u0 = fma(l0[t], cv[t], u0);
+            u1 = fma(l1[t], cv[t], u1);
+          }
         }
       }
-      if (j < n) {
-        const int dst = j / per;
-        const unsigned b = rbar(kMbColp, dst);
-        const unsigned p0 = raddr(&sh.colp_in[rk][j - dst * per][0], dst);
-        st_async2(p0, u, v0, b);
-        st_async2(p0 + 16, v1, v2, b);
-      }
+      const int dst = j0 / per;
+      st_async2(raddr(&sh.colp_in[rk][j0 - dst * per], dst), u0, u1, rbar(kMbColp, dst));
     }
     wait(kMbColp);
     pc.mark(15);
-    // my column slice: fold the 16 partials (fixed order), new Li row n
-    // entries to its owner, new weights to every CTA
+    expect(kMbW, (unsigned)(kClusterCTAs * per * 8));
+    for (int e = tid; e < (per / 2) * kClusterCTAs; e += kLoopThreads) {  // fold + all-gather
+      const int jj = 2 * (e / kClusterCTAs), dst = e % kClusterCTAs;
+      double u0 = 0.0, u1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < kClusterCTAs; ++q) {  // fixed order
+        u0 += sh.colp_in[q][jj];
+        u1 += sh.colp_in[q][jj + 1];
+      }
+      st_async2(raddr(&sh.u_all[jlo + jj], dst), u0, u1, rbar(kMbW, dst));
+    }
     const int owner = n % kClusterCTAs, qn = n / kClusterCTAs;
-    expect(kMbW, (unsigned)(n * 24 + (owner == rk ? n * 8 : 0)));
     double* Lirow_g = a.Li + tri_off(n);
     double* wgt = a.sup + 3 * (int64_t)cap;
-    for (int e = tid; e < (jhi - jlo) * 4; e += kLoopThreads) {  // fixed-order fold
-      const int jj = e >> 2, c = e & 3;
-      double part[kClusterCTAs];
-#pragma unroll
-      for (int q = 0; q < kClusterCTAs; ++q) part[q] = sh.colp_in[q][jj][c];
-      double t = 0.0;
-#pragma unroll
-      for (int q = 0; q < kClusterCTAs; ++q) t += part[q];
-      cm.red[e] = t;
-    }
-    __syncthreads();
-    for (int e = tid; e < (jhi - jlo) * kClusterCTAs; e += kLoopThreads) {
-      const int jj = e / kClusterCTAs, dst = e % kClusterCTAs, j = jlo + jj;
-      const double lij = -cm.red[4 * jj] / l;
-      const double w0 = fma(lij, yn0, cm.red[4 * jj + 1]), w1 = fma(lij, yn1, cm.red[4 * jj + 2]),
-                   w2 = fma(lij, yn2, cm.red[4 * jj + 3]);
-      const unsigned b = rbar(kMbW, dst);
-      st_async(raddr(&sh.wx[j], dst), w0, b);
-      st_async(raddr(&sh.wy[j], dst), w1, b);
-      st_async(raddr(&sh.wz[j], dst), w2, b);
-      if (dst == owner) st_async(raddr(&sh.Liown[own_off(qn, owner) + j], dst), lij, b);
-      if (dst == 0) {
-        Lirow_g[j] = lij;
-        wgt[j] = w0;
-        wgt[cap + j] = w1;
-        wgt[2 * cap + j] = w2;
-      }
-    }
     // the new support, in every CTA's resident copy
     if (tid == 0) {
       sh.ux[n] = px;
@@ -1435,6 +1410,20 @@ struct MsgPath {
       }
     }
     wait(kMbW);
+    const double neg_inv_l = -1.0 / l;
+    for (int j = tid; j < n; j += kLoopThreads) {  // x' = x + Li[n][j] y_n
+      const double lij = sh.u_all[j] * neg_inv_l;
+      sh.wx[j] = fma(lij, yn0, sh.wx[j]);
+      sh.wy[j] = fma(lij, yn1, sh.wy[j]);
+      sh.wz[j] = fma(lij, yn2, sh.wz[j]);
+      if (rk == owner) sh.Liown[own_off(qn, owner) + j] = lij;
+      if (j >= jlo && j < jlo + per) {  // my slice -> global copies
+        wgt[j] = sh.wx[j];
+        wgt[cap + j] = sh.wy[j];
+        wgt[2 * cap + j] = sh.wz[j];
+        Lirow_g[j] = lij;
+      }
+    }
     if (tid == 0) {
       sh.wx[n] = yn0 / l;
       sh.wy[n] = yn1 / l;

@@ -101,6 +101,47 @@ __global__ void stasync_kernel(int iters, unsigned long long* out) {
   c.sync();
 }
 
+// all-to-all volume test: each CTA pushes `per` values (8 B each, or 16 B
+// pairs) to every CTA per round, spread over threads; waits for its own.
+template <bool V2>
+__global__ void stasync_volume_kernel(int iters, int per, unsigned long long* out, int slot) {
+  __shared__ double buf[16 * 64];
+  __shared__ __align__(8) unsigned long long mbar[2];
+  cg::cluster_group c = cg::this_cluster();
+  const unsigned rank = c.block_rank();
+  if (threadIdx.x < 2) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&mbar[threadIdx.x])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  c.sync();
+  const int msgs = V2 ? per / 2 : per;   // per destination
+  const unsigned bytes_in = 16 * per * 8;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    const int b = i & 1;
+    const unsigned parity = (i >> 1) & 1;
+    if (threadIdx.x == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(&mbar[b])), "r"(bytes_in) : "memory");
+    for (int e = threadIdx.x; e < 16 * msgs; e += blockDim.x) {
+      const int dst = e % 16, k = e / 16;
+      unsigned raddr, rbar;
+      const unsigned laddr = smem_u32(&buf[rank * 64 + (V2 ? 2 * k : k)]);
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(laddr), "r"(dst));
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(&mbar[b])), "r"(dst));
+      const double v = (double)i;
+      if (V2)
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" :: "r"(raddr), "d"(v), "d"(v), "r"(rbar) : "memory");
+      else
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" :: "r"(raddr), "d"(v), "r"(rbar) : "memory");
+    }
+    unsigned done = 0;
+    while (!done) {
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(smem_u32(&mbar[b])), "r"(parity) : "memory");
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[slot] = (unsigned long long)(clock64() - t0);
+  c.sync();
+}
+
 int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   rbf::GridBarrier* bar; int* fault; unsigned long long* out;
@@ -141,6 +182,21 @@ int main() {
     cudaError_t e2 = cudaLaunchKernelEx(&cfg, stasync_kernel, iters, out);
     if (e2 != cudaSuccess) printf("stasync launch: %s\n", cudaGetErrorString(e2));
   }
+  unsigned long long* out2; cudaMalloc(&out2, 16 * 8); cudaMemset(out2, 0, 16 * 8);
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(16); cfg.blockDim = dim3(512);
+    cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 16; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    cudaFuncSetAttribute(stasync_volume_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(stasync_volume_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    int pers[4] = {2, 8, 18, 28};
+    for (int q = 0; q < 4; ++q) {
+      cudaLaunchKernelEx(&cfg, stasync_volume_kernel<false>, 2000, pers[q], out2, q);
+      cudaLaunchKernelEx(&cfg, stasync_volume_kernel<true>, 2000, pers[q], out2, 4 + q);
+    }
+  }
   timer_kernel<<<1, 1>>>(out, 1000);
   int n = 1 << 16; int* next; cudaMalloc(&next, n * 4);
   int* h = new int[n]; for (int i = 0; i < n; ++i) h[i] = (i * 7919 + 13) % n;
@@ -156,6 +212,12 @@ int main() {
   printf("st.async x16 + mbarrier wait:        %.1f cycles/round\n", r[3] / (double)iters);
   printf("L2 dependent load latency:           %.1f ns\n", r[5] / 20000.0);
   printf("DSMEM store x16 + cluster sync:      %.1f cycles\n", r[4] / (double)iters);
+  {
+    unsigned long long r2[16]; cudaMemcpy(r2, out2, 16 * 8, cudaMemcpyDeviceToHost);
+    int pers[4] = {2, 8, 18, 28};
+    for (int q = 0; q < 4; ++q)
+      printf("all-to-all %2d doubles/CTA-pair: b64 %.0f cyc, v2 %.0f cyc per round\n", pers[q], r2[q] / 2000.0, r2[4 + q] / 2000.0);
+  }
   printf("globaltimer read:                    %.1f cycles\n", r[6] / 1000.0);
   printf("clock64 read:                        %.1f cycles\n", r[7] / 1000.0);
   return 0;
