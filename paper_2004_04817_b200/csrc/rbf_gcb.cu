@@ -48,6 +48,7 @@ constexpr int kSupTile = 2048;       // GlobalPath: supports staged per scan til
 constexpr int kRowSmemMax = 8192;    // GlobalPath: row held in shared memory
 constexpr int kSmallMax = 1024;      // SmemPath: supports resident in shared memory
 constexpr int kAutoClusterMaxCard = 2048;
+constexpr int64_t kClusterScanPairs = 400000;  // per group scan, see gcb_driver
 constexpr int kNone = 0x7fffffff;
 
 struct LoopScratch {
@@ -1574,6 +1575,13 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
     if (n >= a.max_supports) {
       done_loop = 1;
       break;
+    }
+    // one-cluster paths hand over to the whole-GPU grid once a group scan
+    // (card x n pairs on 16 SMs) costs more than the grid's extra barriers
+    if (self_mode != RBF_GCB_GRID && self_mode != RBF_GCB_CLUSTER &&
+        (int64_t)((a.nb + m - 1) / m) * n > kClusterScanPairs) {
+      save(RBF_EGROW, RBF_GCB_GRID);
+      return;
     }
     if (n >= Path::kMaxN - 1) {  // beyond this path's resident capacity
       save(RBF_EGROW, self_mode == RBF_GCB_MSG ? RBF_GCB_SMEM

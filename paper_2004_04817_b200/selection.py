@@ -366,6 +366,12 @@ def _gcb_run(boundary, config, mode=None):
 
     ctas = N.ctypes.c_int32(0)
     resolved = N.ctypes.c_int32(0)
+    if mode is None:  # RBF_GCB_MODE=msg|smem|cluster|grid overrides the automatic choice
+        import os
+
+        name = os.environ.get("RBF_GCB_MODE", "").lower()
+        mode = {"msg": N.GCB_MSG, "smem": N.GCB_SMEM, "cluster": N.GCB_CLUSTER,
+                "grid": N.GCB_GRID}.get(name)
     want = N.GCB_AUTO if mode is None else mode
     N.check(lib.rbf_gcb_ctas(want, nb, m, N.ctypes.byref(ctas), N.ctypes.byref(resolved)),
             "rbf_gcb_ctas")
