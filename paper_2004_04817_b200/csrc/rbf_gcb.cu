@@ -940,13 +940,14 @@ struct SmemPath {
 // cycles measured, tools/barrier_bench.cu). Factor rows are owner-stable:
 // row i of L and Li lives in CTA i % 16 (packed), so the n < kMsgMax rows of
 // both factors fit next to the replicated vectors.
-constexpr int kMsgMax = 448;
-constexpr int kMsgOwnRows = kMsgMax / kClusterCTAs;                 // 28
+constexpr int kMsgMax = 384;
+constexpr int kMsgOwnRows = kMsgMax / kClusterCTAs;                 // 24
 constexpr int kMsgOwnElems = 8 * kMsgOwnRows * (kMsgOwnRows - 1) + kMsgOwnRows * kClusterCTAs;
-constexpr int kMsgSlice = (kMsgMax + kClusterCTAs - 1) / kClusterCTAs;  // 28 columns
+// column-owned copy of Li: column j = 16 q + rank holds rows j .. kMsgMax-1
+constexpr int kMsgColElems = kMsgOwnRows * kMsgMax - 8 * kMsgOwnRows * (kMsgOwnRows - 1);
 constexpr int kMsgGoff = 512;   // group offsets cached in shared memory (else read from L2)
 
-enum MsgBar { kMbScan0 = 0, kMbScan1, kMbC0, kMbR, kMbC1, kMbColp, kMbW, kMbCount };
+enum MsgBar { kMbScan0 = 0, kMbScan1, kMbC0, kMbR, kMbC1, kMbW, kMbCount };
 
 struct MsgShared {
   Common cm;
@@ -956,8 +957,8 @@ struct MsgShared {
   double y0[kMsgMax], y1[kMsgMax], y2[kMsgMax];  // forward-substituted d
   double row[kMsgMax], c0[kMsgMax], r[kMsgMax], c1[kMsgMax];
   double Lown[kMsgOwnElems], Liown[kMsgOwnElems];  // owned rows i = 16 q + rank
-  alignas(16) double colp_in[kClusterCTAs][kMsgSlice];  // u partials for my slice
-  alignas(16) double u_all[kMsgMax];                     // u = Li^T c, all-gathered
+  double Licol[kMsgColElems];                      // owned columns of Li
+  double u_all[kMsgMax];                           // u = Li^T c, all-gathered
   double rpart[kClusterCTAs][4];                   // c.c, c.y partials
   double part_in[2][kClusterCTAs][2][2];           // scan partials (err, pos as double)
   double acc[kLoopWarps][4][4];
@@ -1001,6 +1002,10 @@ struct MsgPath {
   __device__ int rank() const { return blockIdx.x; }
 
   __device__ static int own_off(int q, int rank) { return 8 * q * (q - 1) + q * (rank + 1); }
+  // column j = 16 qc + rank, capacity kMsgMax - j entries (rows j ..)
+  __device__ static int own_col_off(int qc, int rank) {
+    return qc * (kMsgMax - rank) - 8 * qc * (qc - 1);
+  }
 
   // -------------------------------------------------------------- mbarriers
   __device__ void expect(int bar, unsigned bytes) {
@@ -1062,13 +1067,14 @@ struct MsgPath {
       sh.y1[j] = __ldcg(a.y + 3 * j + 1);
       sh.y2[j] = __ldcg(a.y + 3 * j + 2);
     }
-    // owned factor rows i = 16 q + rank < n
+    // owned factor rows i = 16 q + rank < n, owned columns of Li
     for (int q = 0; 16 * q + rk < n; ++q) {
-      const int i = 16 * q + rk, o = own_off(q, rk);
+      const int i = 16 * q + rk, o = own_off(q, rk), oc = own_col_off(q, rk);
       for (int j = threadIdx.x; j <= i; j += kLoopThreads) {
         sh.Lown[o + j] = __ldcg(a.L + tri_off(i) + j);
         sh.Liown[o + j] = __ldcg(a.Li + tri_off(i) + j);
       }
+      for (int r = i + threadIdx.x; r < n; r += kLoopThreads) sh.Licol[oc + (r - i)] = __ldcg(a.Li + tri_off(r) + i);
     }
     for (int g = threadIdx.x; g <= a.m && g <= kMsgGoff; g += kLoopThreads) sh.goff[g] = __ldg(a.group_off + g);
     __syncthreads();
@@ -1324,51 +1330,35 @@ struct MsgPath {
     const double yn2 = (__ldg(a.disp + 3 * (int64_t)pos + 2) - cm.dbl[4]) / l;
     // u = Li^T c (the weights are updated incrementally,
     // x' = x - (u / l) y_n: as accurate as recomputing Li^T y).
-    // Reduce-scatter: partial u over the owned rows, column pairs pushed to
-    // the CTA folding that slice; all-gather: each slice of u to every CTA.
-    const int per = 2 * ((n + 2 * kClusterCTAs - 1) / (2 * kClusterCTAs));  // even
-    const int jlo = rk * per;
-    expect(kMbColp, (unsigned)(kClusterCTAs * per * 8));
-    const int nown = n > rk ? (n - rk + kClusterCTAs - 1) / kClusterCTAs : 0;
-    for (int jp = tid; 2 * jp < kClusterCTAs * per; jp += kLoopThreads) {
-      const int j0 = 2 * jp;
-      double u0 = 0.0, u1 = 0.0;
-      if (j0 < n) {
-        const int q0 = j0 > rk ? (j0 - rk + kClusterCTAs - 1) / kClusterCTAs : 0;
-        for (int qb = q0; qb < nown; qb += 4) {
-          double l0[4], l1[4], cv[4];
+    // Li is also kept column-owned (column j in CTA j % 16), so u_j is a
+    // local dot product of column j with the replicated c; one all-gather
+    // hands u to every CTA. The column owner appends Li[n][j] = -u_j / l.
+    const double neg_inv_l = -1.0 / l;
+    expect(kMbW, (unsigned)(n * 8));
+    for (int qc = warp; 16 * qc + rk < n; qc += kLoopWarps) {
+      const int j = 16 * qc + rk;
+      const double* col = sh.Licol + own_col_off(qc, rk);
+      double acc0 = 0.0, acc1 = 0.0;
+      for (int i0 = j; i0 < n; i0 += 8 * kWarp) {
+        double lv[8], cv[8];
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int q = qb + t, i = 16 * q + rk;
-            const bool ok = q < nown;
-            const int o = own_off(ok ? q : 0, rk);
-            l0[t] = ok ? sh.Liown[o + j0] : 0.0;
-            l1[t] = (ok && j0 + 1 <= i) ? sh.Liown[o + j0 + 1] : 0.0;
-            cv[t] = ok ? sh.c1[i] : 0.0;
-          }
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u * kWarp + lane;
+          lv[u] = i < n ? col[i - j] : 0.0;
+          cv[u] = i < n ? sh.c1[i] : 0.0;
+        }
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            u0 = fma(l0[t], cv[t], u0);
-            u1 = fma(l1[t], cv[t], u1);
-          }
+        for (int u = 0; u < 8; u += 2) {
+          acc0 = fma(lv[u], cv[u], acc0);
+          acc1 = fma(lv[u + 1], cv[u + 1], acc1);
         }
       }
-      const int dst = j0 / per;
-      st_async2(raddr(&sh.colp_in[rk][j0 - dst * per], dst), u0, u1, rbar(kMbColp, dst));
+      const double uj = warp_sum(acc0 + acc1);
+      bcast(sh.u_all, j, uj, kMbW, lane);
+      if (lane == 0) sh.Licol[own_col_off(qc, rk) + (n - j)] = uj * neg_inv_l;
     }
-    wait(kMbColp);
+    if (n % kClusterCTAs == rk && tid == 0) sh.Licol[own_col_off(n / kClusterCTAs, rk)] = 1.0 / l;
     pc.mark(15);
-    expect(kMbW, (unsigned)(kClusterCTAs * per * 8));
-    for (int e = tid; e < (per / 2) * kClusterCTAs; e += kLoopThreads) {  // fold + all-gather
-      const int jj = 2 * (e / kClusterCTAs), dst = e % kClusterCTAs;
-      double u0 = 0.0, u1 = 0.0;
-#pragma unroll
-      for (int q = 0; q < kClusterCTAs; ++q) {  // fixed order
-        u0 += sh.colp_in[q][jj];
-        u1 += sh.colp_in[q][jj + 1];
-      }
-      st_async2(raddr(&sh.u_all[jlo + jj], dst), u0, u1, rbar(kMbW, dst));
-    }
     const int owner = n % kClusterCTAs, qn = n / kClusterCTAs;
     double* Lirow_g = a.Li + tri_off(n);
     double* wgt = a.sup + 3 * (int64_t)cap;
@@ -1411,14 +1401,13 @@ struct MsgPath {
       }
     }
     wait(kMbW);
-    const double neg_inv_l = -1.0 / l;
     for (int j = tid; j < n; j += kLoopThreads) {  // x' = x + Li[n][j] y_n
       const double lij = sh.u_all[j] * neg_inv_l;
       sh.wx[j] = fma(lij, yn0, sh.wx[j]);
       sh.wy[j] = fma(lij, yn1, sh.wy[j]);
       sh.wz[j] = fma(lij, yn2, sh.wz[j]);
       if (rk == owner) sh.Liown[own_off(qn, owner) + j] = lij;
-      if (j >= jlo && j < jlo + per) {  // my slice -> global copies
+      if (j % kClusterCTAs == rk) {  // my columns -> global copies
         wgt[j] = sh.wx[j];
         wgt[cap + j] = sh.wy[j];
         wgt[2 * cap + j] = sh.wz[j];
