@@ -188,8 +188,12 @@ typedef struct rbf_gcb_args {
   const int32_t* group_pos; /* (nb) positions, groups concatenated        */
   const int32_t* group_off; /* (m + 1) offsets into group_pos              */
   int32_t nb, m;
-  int32_t mode;             /* RBF_GCB_AUTO / _CLUSTER / _GRID             */
+  int32_t mode;             /* RBF_GCB_AUTO / _CLUSTER / _GRID / ...       */
   int32_t max_supports;
+  int32_t clusters;         /* MSG path: 16-CTA clusters sharing the group
+                               scans (0 = library default); each computes the
+                               appends redundantly, scan partials meet in L2 */
+  int32_t reserved;
   double radius, tol;
   double dup_dist;          /* NEAR_DUPLICATE_FRACTION * radius            */
   /* factor state (device), capacity in rows */

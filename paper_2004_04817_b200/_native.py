@@ -87,6 +87,8 @@ class GcbArgs(ctypes.Structure):
         ("m", ctypes.c_int32),
         ("mode", ctypes.c_int32),
         ("max_supports", ctypes.c_int32),
+        ("clusters", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
         ("radius", ctypes.c_double),
         ("tol", ctypes.c_double),
         ("dup_dist", ctypes.c_double),

@@ -49,6 +49,7 @@ constexpr int kRowSmemMax = 8192;    // GlobalPath: row held in shared memory
 constexpr int kSmallMax = 1024;      // SmemPath: supports resident in shared memory
 constexpr int kAutoClusterMaxCard = 2048;
 constexpr int64_t kClusterScanPairs = 400000;  // per group scan, see gcb_driver
+constexpr int kMsgDefaultClusters = 1;         // MSG path: clusters sharing the scans
 constexpr int kNone = 0x7fffffff;
 
 struct LoopScratch {
@@ -63,6 +64,8 @@ struct LoopScratch {
   double* c1;      // [cap]
   double* gpt;     // [nb][3] boundary points in group order
   double* gdisp;   // [nb][3] displacements in group order
+  double* xc;      // [2 parities][16 clusters][4]: per-cluster (err, pos) x 2
+  unsigned* xseq;  // [2][16] publication sequence numbers
 };
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
@@ -88,6 +91,8 @@ static LoopScratch carve(void* base, int nb, int cap, int ctas, size_t* total) {
   s.c1 = reinterpret_cast<double*>(take(sizeof(double) * (size_t)cap));
   s.gpt = reinterpret_cast<double*>(take(sizeof(double) * 3 * (size_t)nb));
   s.gdisp = reinterpret_cast<double*>(take(sizeof(double) * 3 * (size_t)nb));
+  s.xc = reinterpret_cast<double*>(take(sizeof(double) * 2 * 16 * 4));
+  s.xseq = reinterpret_cast<unsigned*>(take(sizeof(unsigned) * 2 * 16));
   if (total) *total = off;
   return s;
 }
@@ -999,7 +1004,10 @@ struct MsgPath {
 
   static constexpr int kMaxN = kMsgMax;
   __device__ Common& cm() { return sh.cm; }
-  __device__ int rank() const { return blockIdx.x; }
+  unsigned gathers;  // publications so far (cross-cluster sequence numbers)
+  __device__ int rank() const { return blockIdx.x % kClusterCTAs; }
+  __device__ int cluster() const { return blockIdx.x / kClusterCTAs; }
+  __device__ int nclusters() const { return gridDim.x / kClusterCTAs; }
 
   __device__ static int own_off(int q, int rank) { return 8 * q * (q - 1) + q * (rank + 1); }
   // column j = 16 qc + rank, capacity kMsgMax - j entries (rows j ..)
@@ -1042,7 +1050,14 @@ struct MsgPath {
   __device__ __forceinline__ unsigned raddr(const void* p, int dst) { return mapa(smem_u32(p), dst); }
   __device__ __forceinline__ unsigned rbar(int bar, int dst) { return mapa(smem_u32(&sh.mbar[bar]), dst); }
 
-  __device__ void sync() { cg::this_cluster().sync(); }
+  // rare-path / exit barrier: the whole team (all clusters) when there are
+  // several (the launch is cooperative), else the cluster
+  __device__ void sync() {
+    if (nclusters() > 1)
+      cg::this_grid().sync();
+    else
+      cg::this_cluster().sync();
+  }
 
   __device__ void begin(int n) {
     const int cap = a.cap, rk = rank();
@@ -1107,14 +1122,51 @@ struct MsgPath {
       if (lane == 0) sh.cm.bcast[slot] = b;
     }
     __syncthreads();
+    const int ncl = nclusters();
+    if (ncl > 1) {  // combine the clusters' results through L2
+      const unsigned seq = ++gathers;
+      if (rank() == 0 && threadIdx.x == 0) {
+        double* slot = s.xc + (par * 16 + cluster()) * 4;
+        slot[0] = sh.cm.bcast[0].err;
+        slot[1] = (double)sh.cm.bcast[0].pos;
+        slot[2] = sh.cm.bcast[1].err;
+        slot[3] = (double)sh.cm.bcast[1].pos;
+        __threadfence();
+        st_release(s.xseq + par * 16 + cluster(), seq);
+      }
+      if (threadIdx.x < 32 * nslots) {
+        const int slot = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        Best b{-1.0, kNone};
+        if (lane < ncl) {
+          uint64_t t0 = 0;
+          unsigned spins = 0;
+          while (ld_acquire(s.xseq + par * 16 + lane) != seq) {
+            if ((++spins & 1023u) == 0) {
+              const uint64_t now = globaltimer_ns();
+              if (t0 == 0) {
+                t0 = now;
+              } else if (now - t0 > 20ull * 1000000000ull) {
+                atomicExch(s.fault, 3);
+                __trap();
+              }
+            }
+          }
+          const double* x = s.xc + (par * 16 + lane) * 4;
+          b = Best{__ldcg(x + 2 * slot), (int)__ldcg(x + 2 * slot + 1)};
+        }
+        b = warp_best(b);
+        if (lane == 0) sh.cm.bcast[slot] = b;
+      }
+      __syncthreads();
+    }
   }
 
   // -------------------------------------------------------------------- scan
   // targets per lane chosen so the CTA's rows fill as many warps as possible
   __device__ void scan(const int* gpos, const double* gpt, const double* gdisp, int card, int n,
                        int par) {
-    const int lo = (int)((int64_t)card * blockIdx.x / kClusterCTAs);
-    const int hi = (int)((int64_t)card * (blockIdx.x + 1) / kClusterCTAs);
+    const int lo = (int)((int64_t)card * blockIdx.x / gridDim.x);
+    const int hi = (int)((int64_t)card * (blockIdx.x + 1) / gridDim.x);
     const int mine = hi - lo;
     if (mine <= kLoopWarps)
       scan_t<1>(gpos, gpt, gdisp, lo, hi, n, par);
@@ -1374,7 +1426,7 @@ struct MsgPath {
       sh.y1[n] = yn1;
       sh.y2[n] = yn2;
       a.inel[pos] = 1;
-      if (rk == 0) {  // global copies
+      if (rk == 0 && cluster() == 0) {  // global copies
         a.y[3 * (int64_t)n] = yn0;
         a.y[3 * (int64_t)n + 1] = yn1;
         a.y[3 * (int64_t)n + 2] = yn2;
@@ -1391,9 +1443,10 @@ struct MsgPath {
     }
     if (rk == owner) {  // row n of L = [c, l] (c replicated), diagonal of Li
       const int o = own_off(qn, owner);
+      const bool global_copy = cluster() == 0;
       for (int j = tid; j < n; j += kLoopThreads) {
         sh.Lown[o + j] = sh.c1[j];
-        a.L[tri_off(n) + j] = sh.c1[j];
+        if (global_copy) a.L[tri_off(n) + j] = sh.c1[j];
       }
       if (tid == 0) {
         sh.Lown[o + n] = l;
@@ -1407,7 +1460,7 @@ struct MsgPath {
       sh.wy[j] = fma(lij, yn1, sh.wy[j]);
       sh.wz[j] = fma(lij, yn2, sh.wz[j]);
       if (rk == owner) sh.Liown[own_off(qn, owner) + j] = lij;
-      if (j % kClusterCTAs == rk) {  // my columns -> global copies
+      if (j % kClusterCTAs == rk && cluster() == 0) {  // my columns -> global copies
         wgt[j] = sh.wx[j];
         wgt[cap + j] = sh.wy[j];
         wgt[2 * cap + j] = sh.wz[j];
@@ -1711,7 +1764,7 @@ __global__ void __launch_bounds__(kLoopThreads, 1) gcb_msg_kernel(rbf_gcb_args a
   MsgShared& sh = *reinterpret_cast<MsgShared*>(g_smem);
   PhaseClock pc;
   pc.start(sh.cm.phase);
-  MsgPath P{a, s, sh, 1.0 / a.radius, pc, 0u};
+  MsgPath P{a, s, sh, 1.0 / a.radius, pc, 0u, 0u};
   gcb_driver(P, a, s, pc, RBF_GCB_MSG);
   P.finish();
 }
@@ -1723,23 +1776,25 @@ static int resolve_mode(int mode, int nb, int m) {
 }
 
 static cudaError_t launch_cluster(const void* fn, rbf_gcb_args& a, LoopScratch& s, size_t smem,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, int nclusters = 1) {
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(kClusterCTAs);
+  cfg.gridDim = dim3(kClusterCTAs * nclusters);
   cfg.blockDim = dim3(kLoopThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = kClusterCTAs;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeCooperative;  // several clusters wait on each other
+  at[1].val.cooperative = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = nclusters > 1 ? 2 : 1;
   void* args[] = {&a, &s};
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
@@ -1796,7 +1851,13 @@ extern "C" int rbf_gcb_run(const rbf_gcb_args* args, void* stream) {
   RBF_CUDA_TRY(cudaMemsetAsync(s.bar, 0, 64, st));
   rbf_gcb_args acopy = a;
   if (mode == RBF_GCB_MSG) {
-    RBF_CUDA_TRY(launch_cluster((const void*)gcb_msg_kernel, acopy, s, sizeof(MsgShared), st));
+    int dev = 0;
+    RBF_CUDA_TRY(cudaGetDevice(&dev));
+    const int max_cl = sm_count(dev) / kClusterCTAs;
+    int ncl = a.clusters > 0 ? a.clusters : kMsgDefaultClusters;
+    ncl = ncl < 1 ? 1 : (ncl > max_cl ? max_cl : (ncl > 16 ? 16 : ncl));
+    RBF_CUDA_TRY(cudaMemsetAsync(s.xseq, 0, sizeof(unsigned) * 2 * 16, st));
+    RBF_CUDA_TRY(launch_cluster((const void*)gcb_msg_kernel, acopy, s, sizeof(MsgShared), st, ncl));
   } else if (mode == RBF_GCB_SMEM) {
     RBF_CUDA_TRY(launch_cluster((const void*)gcb_smem_kernel, acopy, s, sizeof(SmemShared), st));
   } else if (mode == RBF_GCB_CLUSTER) {

@@ -387,6 +387,9 @@ def _gcb_run(boundary, config, mode=None):
     args.nb, args.m = nb, m
     args.mode = resolved.value
     args.max_supports = int(min(config.max_supports, 2**31 - 1))
+    import os
+
+    args.clusters = int(os.environ.get("RBF_GCB_CLUSTERS", "0"))
     args.radius = radius
     args.tol = float(config.tol)
     args.dup_dist = NEAR_DUPLICATE_FRACTION * config.radius

@@ -407,3 +407,21 @@ def test_selection_cluster_and_grid_modes(cuda, name):
         assert np.array_equal(res.support.nodes, g["seq"]), mode
         assert [r.node for r in res.history.records] == g["rec_node"].tolist()
         assert rel(res.support.weights, g["weights"]) <= 1e-9
+
+
+def test_selection_multi_cluster_msg_path(cuda, monkeypatch):
+    """The message-passing path with several 16-CTA clusters sharing the
+    group scans (redundant appends, scan partials combined through L2)
+    reproduces the reference too (an experimental launch shape)."""
+    from paper_2004_04817_b200 import _native as N
+    from paper_2004_04817_b200.selection import _gcb_run
+
+    monkeypatch.setenv("RBF_GCB_CLUSTERS", "2")
+    g = load_golden("cfg0_m8")
+    pts, disp, _ = golden_inputs("cfg0_m8", g)
+    radius, tol, cap, m, seed = g["params"]
+    b = cuda.BoundarySet(np.arange(len(pts)), pts, disp)
+    cfg = cuda.SelectionConfig(radius=radius, tol=tol, max_supports=int(cap), m=int(m), seed=int(seed))
+    res = _gcb_run(b, cfg, mode=N.GCB_MSG)
+    assert np.array_equal(res.support.nodes, g["seq"])
+    assert rel(res.support.weights, g["weights"]) <= 1e-9
