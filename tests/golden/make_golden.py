@@ -143,6 +143,15 @@ def main():
     out, res = run_selection(wl.points, wl.disp, wl.radius, wl.tol, wl.nb, 32, 0)
     vidx, u = volume_sample(wl, res.support, wl.radius)
     save("cfg1_m32", digest=np.array(digest(wl.points, wl.disp, wl.volume)), vol_idx=vidx, vol_u=u, **out)
+    wl = W.config(2, nv=200_000)  # BASELINE configs[2] at full boundary size
+    out, res = run_selection(wl.points, wl.disp, wl.radius, wl.tol, wl.nb, 48, 0)
+    vidx, u = volume_sample(wl, res.support, wl.radius)
+    save("cfg2_m48", digest=np.array(digest(wl.points, wl.disp)), vol_idx=vidx, vol_u=u, **out)
+    # BASELINE configs[3] at full boundary size (Nb = 200k, m = 64, R = 4), first 400 supports
+    wl = W.config(3, nv=100_000)
+    out, res = run_selection(wl.points, wl.disp, wl.radius, wl.tol, 400, 64, 0)
+    vidx, u = volume_sample(wl, res.support, wl.radius)
+    save("cfg3_m64_cap400", digest=np.array(digest(wl.points, wl.disp)), vol_idx=vidx, vol_u=u, **out)
     wl = W.structured_wing(n_span=60, n_section=200, nv=100_000, m=48, name="cfg2s")
     out, res = run_selection(wl.points, wl.disp, wl.radius, wl.tol, wl.nb, 48, 0)
     vidx, u = volume_sample(wl, res.support, wl.radius)

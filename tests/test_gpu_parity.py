@@ -10,7 +10,8 @@ Tolerances (floating point, FP64 throughout):
   * weights: norm-wise max|dW| / max|W| <= 1e-9 where kappa(Phi) <= 1e8
     (configs 0/1, small cases). At kappa ~ 4e9 (config-2 style grid) two
     backward-stable solves of the same system already differ by ~2e-9
-    norm-wise, so the bar there is 2e-8.
+    norm-wise, so the bar there is 2e-8; at kappa = 2.4e10
+    (config 3, R = 4) they differ by 3e-8 and the bar is 1e-7.
 """
 
 import numpy as np
@@ -240,6 +241,11 @@ GOLDEN_SELECTIONS = [
     ("smooth3_m1", 1e-9), ("smooth3_m5", 1e-9), ("smooth11_m1", 1e-9), ("smooth11_m5", 1e-9),
     ("cfg0_m1", 1e-9), ("cfg0_m8", 1e-9), ("cfg1_m32", 1e-9), ("cfg2s_m48", 2e-8),
     ("switch_m8", 1e-9),  # n = 1200: crosses from the shared-memory path to the L2 path
+    ("cfg2_m48", 2e-8),   # BASELINE configs[2] at full size (Nb = 80k): MSG -> GRID hand-over
+    # configs[3] at full size (Nb = 200k, GRID path), first 400 supports: R = 4 makes Phi
+    # very ill-conditioned (kappa = 2.4e10, |w| up to 1.8e5); two stable solves of the same
+    # system differ by 3e-8 norm-wise (displacements 1.5e-8), so the bar is 1e-7
+    ("cfg3_m64_cap400", 1e-7),
 ]
 
 
@@ -250,6 +256,10 @@ def golden_inputs(name, g):
         wl = W.config(0, nv=100_000)
     elif name.startswith("cfg1"):
         wl = W.config(1, nv=2_000_000)
+    elif name == "cfg2_m48":
+        wl = W.config(2, nv=200_000)
+    elif name.startswith("cfg3"):
+        wl = W.config(3, nv=100_000)
     else:
         wl = W.structured_wing(n_span=60, n_section=200, nv=100_000, m=48, name="cfg2s")
     return wl.points, wl.disp, wl
@@ -271,7 +281,8 @@ def test_selection_matches_reference_golden(cuda, name, wtol):
     assert [r.kernel_evals for r in recs] == g["rec_evals"].tolist()
     assert [r.cum_kernel_evals for r in recs] == g["rec_cum"].tolist()
     lm = np.array([r.local_max_error for r in recs])
-    assert np.abs(lm - g["rec_local_max"]).max() <= 1e-9 * g["rec_local_max"].max()
+    lm_tol = 1e-9 if wtol <= 1e-9 else 1e-8
+    assert np.abs(lm - g["rec_local_max"]).max() <= lm_tol * g["rec_local_max"].max()
     f = res.history.final_sweep
     assert [f.iteration, f.node, f.kernel_evals, f.cum_kernel_evals] == g["final"].tolist()
     assert f.group == -1
@@ -281,7 +292,9 @@ def test_selection_matches_reference_golden(cuda, name, wtol):
     assert np.array_equal(res.support.points, pts[g["seq"]])
     if wl is not None:
         u = cuda.evaluate_displacements(wl.volume[g["vol_idx"]], res.support, radius)
-        assert rel(u, g["vol_u"]) <= 1e-9
+        # displacements: 1e-9 (north_star); at kappa = 2.4e10 (configs[3], R = 4) an
+        # alternative stable solve of the reference's own system moves them by 1.5e-8
+        assert rel(u, g["vol_u"]) <= (1e-9 if wtol <= 2e-8 else 1e-7)
 
 
 def test_selection_determinism_and_greedy_alias(cuda):

@@ -11,7 +11,8 @@ from paper_2004_04817_b200 import workloads as W
 
 SELECTION_CASES = [
     "hemisphere_m1", "hemisphere_m4", "smooth0_m1", "smooth0_m5", "smooth3_m1",
-    "smooth3_m5", "smooth11_m1", "smooth11_m5", "cfg0_m1", "cfg0_m8",
+    "smooth3_m5", "smooth11_m1", "smooth11_m5", "cfg0_m1", "cfg0_m8", "switch_m8",
+    "cfg2_m48", "cfg3_m64_cap400",
 ]
 
 
@@ -22,6 +23,10 @@ def inputs_for(name, g):
         wl = W.config(0, nv=100_000)
     elif name.startswith("cfg1"):
         wl = W.config(1, nv=2_000_000)
+    elif name == "cfg2_m48":
+        wl = W.config(2, nv=200_000)
+    elif name.startswith("cfg3"):
+        wl = W.config(3, nv=100_000)
     else:
         wl = W.structured_wing(n_span=60, n_section=200, nv=100_000, m=48, name="cfg2s")
     return wl.points, wl.disp, wl
