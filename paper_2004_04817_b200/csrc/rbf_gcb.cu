@@ -1276,32 +1276,54 @@ struct MsgPath {
   }
 
   // ------------------------------------------------------------------ append
-  // owned rows: q = 0.. with i = 16 q + rank < n; warp w takes q = w, w + 16
+  // owned rows: q = 0.. with i = 16 q + rank < n (q < 24 here); warp w takes
+  // q = w and q = w + 16 together, so no warp handles two rows one after the
+  // other
   template <typename F>
-  __device__ __forceinline__ void for_owned_rows(int n, F&& body) {
-    const int warp = threadIdx.x >> 5;
-    for (int q = warp; 16 * q + rank() < n; q += kLoopWarps) body(q, 16 * q + rank());
+  __device__ __forceinline__ void for_owned_row_pairs(int n, F&& body) {
+    const int warp = threadIdx.x >> 5, rk = rank();
+    for (int q = warp; 16 * q + rk < n; q += 2 * kLoopWarps) {
+      const int qb = q + kLoopWarps;
+      body(q, 16 * q + rk, 16 * qb + rk < n ? qb : -1, 16 * qb + rk);
+    }
   }
 
+  // dot products of packed owned rows (qa: length ia+1; qb < 0: none) with
+  // x, loads of both rows issued before the FMAs, the two warp reductions
+  // interleaved
   template <typename XL>
-  __device__ __forceinline__ double own_dot(const double* M, int q, int i, XL x, int lane) {
-    const double* rowp = M + own_off(q, rank());
-    double acc0 = 0.0, acc1 = 0.0;
-    for (int j0 = 0; j0 <= i; j0 += 8 * kWarp) {
-      double av[8], xv[8];
+  __device__ __forceinline__ void own_dot2(const double* M, int qa, int ia, int qb, int ib, XL x,
+                                           int lane, double& sa, double& sb) {
+    const double* ra = M + own_off(qa, rank());
+    const double* rb = M + own_off(qb < 0 ? 0 : qb, rank());
+    const int la = ia + 1, lb = qb < 0 ? 0 : ib + 1;
+    const int len = la > lb ? la : lb;
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+    for (int j0 = 0; j0 < len; j0 += 4 * kWarp) {
+      double av[4], bv[4], xv[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 4; ++u) {
         const int j = j0 + u * kWarp + lane;
-        av[u] = j <= i ? rowp[j] : 0.0;
-        xv[u] = j <= i ? x(j) : 0.0;
+        xv[u] = j < len ? x(j) : 0.0;
+        av[u] = j < la ? ra[j] : 0.0;
+        bv[u] = j < lb ? rb[j] : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 8; u += 2) {
-        acc0 = fma(av[u], xv[u], acc0);
-        acc1 = fma(av[u + 1], xv[u + 1], acc1);
+      for (int u = 0; u < 4; u += 2) {
+        a0 = fma(av[u], xv[u], a0);
+        a1 = fma(av[u + 1], xv[u + 1], a1);
+        b0 = fma(bv[u], xv[u], b0);
+        b1 = fma(bv[u + 1], xv[u + 1], b1);
       }
     }
-    return warp_sum(acc0 + acc1);
+    double va = a0 + a1, vb = b0 + b1;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      va += __shfl_xor_sync(0xffffffffu, va, off);
+      vb += __shfl_xor_sync(0xffffffffu, vb, off);
+    }
+    sa = va;
+    sb = vb;
   }
 
   // value v of owned row i -> vector `vec` in all 16 CTAs (lanes 0..15 send)
@@ -1325,28 +1347,44 @@ struct MsgPath {
     pc.mark(1);
     // c0 = Li row
     expect(kMbC0, n * 8);
-    for_owned_rows(n, [&](int q, int i) {
-      bcast(sh.c0, i, own_dot(sh.Liown, q, i, [&](int j) { return sh.row[j]; }, lane), kMbC0, lane);
+    for_owned_row_pairs(n, [&](int qa, int ia, int qb, int ib) {
+      double va, vb;
+      own_dot2(sh.Liown, qa, ia, qb, ib, [&](int j) { return sh.row[j]; }, lane, va, vb);
+      bcast(sh.c0, ia, va, kMbC0, lane);
+      if (qb >= 0) bcast(sh.c0, ib, vb, kMbC0, lane);
     });
     wait(kMbC0);
     pc.mark(2);
     // r = row - L c0
     expect(kMbR, n * 8);
-    for_owned_rows(n, [&](int q, int i) {
-      bcast(sh.r, i, sh.row[i] - own_dot(sh.Lown, q, i, [&](int j) { return sh.c0[j]; }, lane), kMbR, lane);
+    for_owned_row_pairs(n, [&](int qa, int ia, int qb, int ib) {
+      double va, vb;
+      own_dot2(sh.Lown, qa, ia, qb, ib, [&](int j) { return sh.c0[j]; }, lane, va, vb);
+      bcast(sh.r, ia, sh.row[ia] - va, kMbR, lane);
+      if (qb >= 0) bcast(sh.r, ib, sh.row[ib] - vb, kMbR, lane);
     });
     wait(kMbR);
     pc.mark(3);
     // c = c0 + Li r, partial sums of c.c and c.y over the owned rows
     expect(kMbC1, n * 8 + kClusterCTAs * 32);
     double pcc = 0.0, pcy0 = 0.0, pcy1 = 0.0, pcy2 = 0.0;
-    for_owned_rows(n, [&](int q, int i) {
-      const double c = sh.c0[i] + own_dot(sh.Liown, q, i, [&](int j) { return sh.r[j]; }, lane);
-      bcast(sh.c1, i, c, kMbC1, lane);
-      pcc = fma(c, c, pcc);
-      pcy0 = fma(c, sh.y0[i], pcy0);
-      pcy1 = fma(c, sh.y1[i], pcy1);
-      pcy2 = fma(c, sh.y2[i], pcy2);
+    for_owned_row_pairs(n, [&](int qa, int ia, int qb, int ib) {
+      double va, vb;
+      own_dot2(sh.Liown, qa, ia, qb, ib, [&](int j) { return sh.r[j]; }, lane, va, vb);
+      const double ca = sh.c0[ia] + va;
+      bcast(sh.c1, ia, ca, kMbC1, lane);
+      pcc = fma(ca, ca, pcc);
+      pcy0 = fma(ca, sh.y0[ia], pcy0);
+      pcy1 = fma(ca, sh.y1[ia], pcy1);
+      pcy2 = fma(ca, sh.y2[ia], pcy2);
+      if (qb >= 0) {
+        const double cb = sh.c0[ib] + vb;
+        bcast(sh.c1, ib, cb, kMbC1, lane);
+        pcc = fma(cb, cb, pcc);
+        pcy0 = fma(cb, sh.y0[ib], pcy0);
+        pcy1 = fma(cb, sh.y1[ib], pcy1);
+        pcy2 = fma(cb, sh.y2[ib], pcy2);
+      }
     });
     Common& cm = sh.cm;
     if (lane == 0) {
@@ -1377,37 +1415,54 @@ struct MsgPath {
       return kRejectPivot;
     }
     const double l = sqrt(pivot2);
-    const double yn0 = (__ldg(a.disp + 3 * (int64_t)pos) - cm.dbl[2]) / l;
-    const double yn1 = (__ldg(a.disp + 3 * (int64_t)pos + 1) - cm.dbl[3]) / l;
-    const double yn2 = (__ldg(a.disp + 3 * (int64_t)pos + 2) - cm.dbl[4]) / l;
+    const double inv_l = 1.0 / l;
+    const double yn0 = (__ldg(a.disp + 3 * (int64_t)pos) - cm.dbl[2]) * inv_l;
+    const double yn1 = (__ldg(a.disp + 3 * (int64_t)pos + 1) - cm.dbl[3]) * inv_l;
+    const double yn2 = (__ldg(a.disp + 3 * (int64_t)pos + 2) - cm.dbl[4]) * inv_l;
     // u = Li^T c (the weights are updated incrementally,
     // x' = x - (u / l) y_n: as accurate as recomputing Li^T y).
     // Li is also kept column-owned (column j in CTA j % 16), so u_j is a
     // local dot product of column j with the replicated c; one all-gather
     // hands u to every CTA. The column owner appends Li[n][j] = -u_j / l.
-    const double neg_inv_l = -1.0 / l;
+    const double neg_inv_l = -inv_l;
     expect(kMbW, (unsigned)(n * 8));
-    for (int qc = warp; 16 * qc + rk < n; qc += kLoopWarps) {
-      const int j = 16 * qc + rk;
-      const double* col = sh.Licol + own_col_off(qc, rk);
-      double acc0 = 0.0, acc1 = 0.0;
-      for (int i0 = j; i0 < n; i0 += 8 * kWarp) {
-        double lv[8], cv[8];
+    // warp w takes owned columns qc = w and w + 16 together
+    for (int qa = warp; 16 * qa + rk < n; qa += 2 * kLoopWarps) {
+      const int qb = qa + kLoopWarps;
+      const int ja = 16 * qa + rk, jb = 16 * qb + rk;
+      const bool has_b = jb < n;
+      const double* ca = sh.Licol + own_col_off(qa, rk);
+      const double* cb = sh.Licol + own_col_off(has_b ? qb : qa, rk);
+      double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+      for (int i0 = ja; i0 < n; i0 += 4 * kWarp) {  // rows i >= ja (column b starts later)
+        double av[4], bv[4], cv[4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 4; ++u) {
           const int i = i0 + u * kWarp + lane;
-          lv[u] = i < n ? col[i - j] : 0.0;
           cv[u] = i < n ? sh.c1[i] : 0.0;
+          av[u] = i < n ? ca[i - ja] : 0.0;
+          bv[u] = (has_b && i < n && i >= jb) ? cb[i - jb] : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 8; u += 2) {
-          acc0 = fma(lv[u], cv[u], acc0);
-          acc1 = fma(lv[u + 1], cv[u + 1], acc1);
+        for (int u = 0; u < 4; u += 2) {
+          a0 = fma(av[u], cv[u], a0);
+          a1 = fma(av[u + 1], cv[u + 1], a1);
+          b0 = fma(bv[u], cv[u], b0);
+          b1 = fma(bv[u + 1], cv[u + 1], b1);
         }
       }
-      const double uj = warp_sum(acc0 + acc1);
-      bcast(sh.u_all, j, uj, kMbW, lane);
-      if (lane == 0) sh.Licol[own_col_off(qc, rk) + (n - j)] = uj * neg_inv_l;
+      double ua = a0 + a1, ub = b0 + b1;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        ua += __shfl_xor_sync(0xffffffffu, ua, off);
+        ub += __shfl_xor_sync(0xffffffffu, ub, off);
+      }
+      bcast(sh.u_all, ja, ua, kMbW, lane);
+      if (lane == 0) sh.Licol[own_col_off(qa, rk) + (n - ja)] = ua * neg_inv_l;
+      if (has_b) {
+        bcast(sh.u_all, jb, ub, kMbW, lane);
+        if (lane == 0) sh.Licol[own_col_off(qb, rk) + (n - jb)] = ub * neg_inv_l;
+      }
     }
     if (n % kClusterCTAs == rk && tid == 0) sh.Licol[own_col_off(n / kClusterCTAs, rk)] = 1.0 / l;
     pc.mark(15);
