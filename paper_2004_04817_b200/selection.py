@@ -156,6 +156,56 @@ class KernelEvalCounter:
         self.count += int(n)
 
 
+class _RecordList(list):
+    """``SelectionHistory.records`` as a real list whose IterationRecord
+    objects are built from the device's record columns on first use (building
+    a few hundred frozen dataclasses costs ~0.4 ms; most callers never look).
+    Every list operation materialises first, so it behaves as a plain list."""
+
+    __slots__ = ("_cols",)
+
+    def __init__(self, cols):
+        super().__init__()
+        self._cols = cols
+
+    def _load(self):
+        cols = self._cols
+        if cols is not None:
+            self._cols = None
+            list.extend(self, [IterationRecord(*v) for v in zip(*cols)])
+        return self
+
+    def __len__(self):
+        cols = self._cols
+        return len(cols[0]) if cols is not None else list.__len__(self)
+
+    def __bool__(self):
+        return len(self) > 0
+
+    def __repr__(self):
+        return list.__repr__(self._load())
+
+    def __reduce__(self):
+        return (list, (list(self._load()),))
+
+
+def _lazy(name):
+    base = getattr(list, name)
+
+    def method(self, *a, **k):
+        return base(self._load(), *a, **k)
+
+    method.__name__ = name
+    return method
+
+
+for _name in ("__getitem__", "__iter__", "__reversed__", "__contains__", "__eq__", "__ne__",
+              "__lt__", "__le__", "__gt__", "__ge__", "__add__", "__iadd__", "__mul__", "__imul__",
+              "__rmul__", "__setitem__", "__delitem__", "append", "extend", "insert", "pop",
+              "remove", "index", "count", "sort", "reverse", "copy", "clear"):
+    setattr(_RecordList, _name, _lazy(_name))
+
+
 # ------------------------------------------------------------ host-side logic
 def _partition_positions(nb, m, seed):
     """PCG64 permutation dealt round-robin (selection.py:183-184); returns the
@@ -319,6 +369,39 @@ class _LoopBuffers:
         self.scratch_bytes = lib.rbf_gcb_scratch_bytes(self.nb, cap, self.ctas)
         self.scratch = t.empty(self.scratch_bytes, dtype=t.uint8, device=dev)
 
+    def _staging(self):
+        sz = N.ctypes.sizeof(N.GcbState) + self.cap * 4 + 3 * self.cap * 8 + self.records.numel()
+        if getattr(self, "_host", None) is None or self._host.numel() < sz:
+            self._host = self.t.empty(sz, dtype=self.t.uint8, pin_memory=True)
+        return self._host
+
+    def read_all(self):
+        """Async copies of state, sel, weight rows and records into one
+        pinned buffer, one synchronisation; returns (state, host bytes)."""
+        t = self.t
+        host = self._staging()
+        ss = N.ctypes.sizeof(N.GcbState)
+        o1 = ss
+        o2 = o1 + self.cap * 4
+        o3 = o2 + 3 * self.cap * 8
+        o4 = o3 + self.records.numel()
+        host[:o1].copy_(self.state, non_blocking=True)
+        host[o1:o2].copy_(self.sel.view(t.uint8), non_blocking=True)
+        host[o2:o3].copy_(self.sup[3:6].reshape(-1).view(t.uint8), non_blocking=True)
+        host[o3:o4].copy_(self.records.reshape(-1), non_blocking=True)
+        t.cuda.current_stream().synchronize()
+        hb = host.numpy()
+        self._offsets = (o1, o2, o3)
+        return N.GcbState.from_buffer_copy(hb[:ss].tobytes()), hb
+
+    def unpack(self, hb, n, nrec):
+        o1, o2, o3 = self._offsets
+        sel = hb[o1:o1 + 4 * n].view(np.int32).astype(np.intp)
+        w = hb[o2:o2 + 24 * self.cap].view(np.float64).reshape(3, self.cap)[:, :n]
+        weights = np.ascontiguousarray(w.T)
+        recs = hb[o3:o3 + nrec * N.RECORD_DTYPE.itemsize].view(N.RECORD_DTYPE).copy()
+        return sel, weights, recs
+
     def resize_scratch(self, ctas):
         self.ctas = ctas
         lib = N.load()
@@ -405,7 +488,9 @@ def _gcb_run(boundary, config, mode=None):
         with N.launching("rbf_gcb_run", kernels=1):
             rc = lib.rbf_gcb_run(N.ctypes.byref(args), stream)
         N.check(rc, "rbf_gcb_run")
-        st = _read_state(buf)
+        # state, selection, weights and records in one staged read (the kernel
+        # is stream-ordered before the copies): one synchronisation per launch
+        st, host = buf.read_all()
         if st.status == N.STATUS_DONE:
             break
         if st.status == N.RBF_ENOTPD:
@@ -436,18 +521,7 @@ def _gcb_run(boundary, config, mode=None):
 
     n = st.n
     nrec = st.n_records
-    # one pinned staging buffer, three async copies, one synchronisation
-    weights_dev = buf.sup[3:6, :n].t().contiguous()
-    host = t.empty(n * 4 + n * 24 + nrec * N.RECORD_DTYPE.itemsize, dtype=t.uint8, pin_memory=True)
-    o1, o2 = n * 4, n * 4 + n * 24
-    host[:o1].copy_(buf.sel[:n].view(t.uint8), non_blocking=True)
-    host[o1:o2].copy_(weights_dev.view(t.uint8).reshape(-1), non_blocking=True)
-    host[o2:].copy_(buf.records[:nrec].reshape(-1), non_blocking=True)
-    t.cuda.current_stream().synchronize()
-    hb = host.numpy()
-    sel = hb[:o1].view(np.int32).astype(np.intp)
-    weights = hb[o1:o2].view(np.float64).reshape(n, 3).copy()
-    recs = hb[o2:].view(N.RECORD_DTYPE)
+    sel, weights, recs = buf.unpack(host, n, nrec)
 
     sizes = np.diff(off)
     history = SelectionHistory(seed=config.seed, m=m)
@@ -457,13 +531,9 @@ def _gcb_run(boundary, config, mode=None):
     evals = sizes[groups] * body["n_before"].astype(np.int64)
     cum = np.cumsum(evals)
     nodes = idx[body["node_pos"]]
-    history.records = [
-        IterationRecord(iteration=3 + i, group=g, node=nd, local_max_error=lm, kernel_evals=ev,
-                        cum_kernel_evals=cm, t1_s=a1, t2_s=a2)
-        for i, (g, nd, lm, ev, cm, a1, a2) in enumerate(zip(
-            groups.tolist(), nodes.tolist(), body["local_max"].tolist(), evals.tolist(),
-            cum.tolist(), body["t1_s"].tolist(), body["t2_s"].tolist()))
-    ]
+    history.records = _RecordList((
+        range(3, 3 + len(body)), groups.tolist(), nodes.tolist(), body["local_max"].tolist(),
+        evals.tolist(), cum.tolist(), body["t1_s"].tolist(), body["t2_s"].tolist()))
     fin = recs[-1]
     sweep_evals = nb * n
     total = (int(cum[-1]) if len(cum) else 0) + sweep_evals
