@@ -223,6 +223,17 @@ RBF_API size_t rbf_gcb_scratch_bytes(int32_t nb, int32_t cap, int32_t ctas);
 RBF_API int rbf_gcb_run(const rbf_gcb_args* args, void* stream);
 
 /* ---------------------------------------------------------------------
+ * Group partition on the host (replaces selection.py:177-185
+ * `partition_boundary`'s arithmetic): numpy's PCG64 permutation of nb dealt
+ * round-robin into m groups, bit for bit. (state, inc) are the 128-bit
+ * words of numpy.random.default_rng(seed).bit_generator.state, split
+ * hi/lo. Writes group_pos_host[nb] (positions, groups concatenated) and
+ * group_off_host[m + 1]. Host memory, no GPU needed.
+ */
+RBF_API int rbf_partition(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                          int64_t nb, int64_t m, int32_t* group_pos_host, int32_t* group_off_host);
+
+/* ---------------------------------------------------------------------
  * Diagnostics (no reference counterpart): an FP64 DFMA throughput probe
  * used to measure the FP64 peak the roofline fractions are quoted against.
  * `scratch` holds rbf_fp64_probe_scratch_bytes(device) bytes; `flops_host`

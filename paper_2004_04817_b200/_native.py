@@ -129,6 +129,9 @@ SIGNATURES = [
       ctypes.POINTER(ctypes.c_int32)]),
     ("rbf_gcb_scratch_bytes", ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
     ("rbf_gcb_run", ctypes.c_int, [ctypes.POINTER(GcbArgs), c_dp]),
+    ("rbf_partition", ctypes.c_int,
+     [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64,
+      ctypes.c_int64, c_dp, c_dp]),
     ("rbf_fp64_probe_scratch_bytes", ctypes.c_size_t, [ctypes.c_int]),
     ("rbf_fp64_probe", ctypes.c_int, [ctypes.c_int, c_dp, ctypes.POINTER(ctypes.c_double), c_dp]),
 ]

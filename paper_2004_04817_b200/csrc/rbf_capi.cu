@@ -64,3 +64,81 @@ extern "C" int rbf_fp64_probe(int iters, double* scratch, double* flops_host, vo
   if (flops_host) *flops_host = 2.0 * 8.0 * 4.0 * (double)iters * (double)blocks * 256.0;
   return RBF_OK;
 }
+
+// --------------------------------------------------------- group partition
+// numpy's Generator(PCG64).permutation(nb) dealt round-robin into m groups
+// (reference selection.py:183-184: perm = default_rng(seed).permutation(nb),
+// groups[j] = perm[j::m]), restated bit for bit on the host: PCG64 is the
+// 128-bit LCG with XSL-RR output, numpy draws 32-bit values from the low
+// then the high half of each 64-bit output, shuffle() is Fisher-Yates from
+// the top with random_interval()'s masked rejection sampling. The caller
+// passes the seeded 128-bit state and increment (bit_generator.state).
+namespace {
+struct Pcg64 {
+  unsigned __int128 state, inc;
+  bool has32 = false;
+  uint32_t hi32 = 0;
+  uint64_t next64() {
+    const unsigned __int128 mult =
+        ((unsigned __int128)0x2360ED051FC65DA4ull << 64) | (unsigned __int128)0x4385DF649FCCF645ull;
+    state = state * mult + inc;
+    const uint64_t x = (uint64_t)(state >> 64) ^ (uint64_t)state;
+    const unsigned rot = (unsigned)(state >> 122);
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+  }
+  uint32_t next32() {
+    if (has32) {
+      has32 = false;
+      return hi32;
+    }
+    const uint64_t v = next64();
+    has32 = true;
+    hi32 = (uint32_t)(v >> 32);
+    return (uint32_t)(v & 0xffffffffu);
+  }
+  uint64_t interval(uint64_t max) {
+    if (max == 0) return 0;
+    uint64_t mask = max;
+    mask |= mask >> 1;
+    mask |= mask >> 2;
+    mask |= mask >> 4;
+    mask |= mask >> 8;
+    mask |= mask >> 16;
+    mask |= mask >> 32;
+    uint64_t v;
+    if (max <= 0xffffffffull) {
+      while ((v = (next32() & mask)) > max) {
+      }
+    } else {
+      while ((v = (next64() & mask)) > max) {
+      }
+    }
+    return v;
+  }
+};
+}  // namespace
+
+extern "C" int rbf_partition(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                             int64_t nb, int64_t m, int32_t* group_pos_host, int32_t* group_off_host) {
+  if (nb < 1 || m < 1 || m > nb || nb > INT32_MAX || !group_pos_host || !group_off_host)
+    return rbf::set_error(RBF_EARG, "bad partition arguments");
+  Pcg64 g;
+  g.state = ((unsigned __int128)state_hi << 64) | state_lo;
+  g.inc = ((unsigned __int128)inc_hi << 64) | inc_lo;
+  int32_t* perm = new int32_t[nb];
+  for (int64_t i = 0; i < nb; ++i) perm[i] = (int32_t)i;
+  for (int64_t i = nb - 1; i >= 1; --i) {
+    const int64_t j = (int64_t)g.interval((uint64_t)i);
+    const int32_t t = perm[j];
+    perm[j] = perm[i];
+    perm[i] = t;
+  }
+  int64_t o = 0;
+  for (int64_t j = 0; j < m; ++j) {
+    group_off_host[j] = (int32_t)o;
+    for (int64_t i = j; i < nb; i += m) group_pos_host[o++] = perm[i];
+  }
+  group_off_host[m] = (int32_t)o;
+  delete[] perm;
+  return RBF_OK;
+}

@@ -207,6 +207,21 @@ for _name in ("__getitem__", "__iter__", "__reversed__", "__contains__", "__eq__
 
 
 # ------------------------------------------------------------ host-side logic
+def _partition_native(nb, m, seed):
+    """Group positions and offsets from the library's host restatement of
+    numpy's PCG64 permutation (rbf_partition): same bits, ~3x faster than
+    numpy's shuffle plus the slicing. Returns (flat int32, off int32)."""
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    s, inc = st["state"], st["inc"]
+    mask = (1 << 64) - 1
+    flat = np.empty(nb, dtype=np.int32)
+    off = np.empty(m + 1, dtype=np.int32)
+    lib = N.load()
+    N.check(lib.rbf_partition(s >> 64, s & mask, inc >> 64, inc & mask, nb, m,
+                              flat.ctypes.data, off.ctypes.data), "rbf_partition")
+    return flat, off
+
+
 def _partition_positions(nb, m, seed):
     """PCG64 permutation dealt round-robin (selection.py:183-184); returns the
     permutation, the groups' positions concatenated (group j = perm[j::m])
@@ -445,7 +460,7 @@ def _gcb_run(boundary, config, mode=None):
     radius = float(config.radius)
     lib = N.require_cuda()
     t = N.torch()
-    _, flat, off = _partition_positions(nb, m, config.seed)
+    flat, off = _partition_native(nb, m, config.seed)
 
     ctas = N.ctypes.c_int32(0)
     resolved = N.ctypes.c_int32(0)
@@ -459,8 +474,8 @@ def _gcb_run(boundary, config, mode=None):
     N.check(lib.rbf_gcb_ctas(want, nb, m, N.ctypes.byref(ctas), N.ctypes.byref(resolved)),
             "rbf_gcb_ctas")
     pts, disp = _boundary_on_device(boundary)
-    gpos = _to_device(flat.astype(np.int32), dtype=t.int32)
-    goff = _to_device(off.astype(np.int32), dtype=t.int32)
+    gpos = _to_device(flat, dtype=t.int32)
+    goff = _to_device(off, dtype=t.int32)
     cap = _initial_capacity(config, nb)
     buf = _LoopBuffers(nb, cap, 2 * cap + m + 8, ctas.value)
 

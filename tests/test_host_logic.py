@@ -103,3 +103,21 @@ def test_no_cpu_fallback():
         P.gcb_select(b, P.SelectionConfig(radius=1.0, tol=1e-6, max_supports=5))
     with pytest.raises(E.NativeUnavailableError):
         P.CholeskyState().append([1.0])
+
+
+def test_native_pcg64_partition_is_numpy_bits():
+    """rbf_partition (C++ host restatement of numpy's PCG64 permutation +
+    round-robin deal) reproduces numpy bit for bit, incl. large nb where
+    random_interval's rejection loop and the 32-bit buffering matter."""
+    from paper_2004_04817_b200.selection import _partition_native
+
+    rng = np.random.default_rng(2024)
+    cases = [(3, 1, 0), (10, 3, 0), (20000, 32, 0), (80000, 48, 0), (200000, 64, 0)]
+    cases += [(int(rng.integers(3, 5000)), 0, int(rng.integers(0, 2**63))) for _ in range(20)]
+    for nb, m, seed in cases:
+        m = m or int(rng.integers(1, nb + 1))
+        flat, off = _partition_native(nb, m, seed)
+        groups = O.partition(nb, m, seed)
+        assert off[-1] == nb
+        for j in range(m):
+            assert np.array_equal(flat[off[j]:off[j + 1]], groups[j]), (nb, m, seed)
