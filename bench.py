@@ -365,7 +365,7 @@ def run_ours(args, rank, world, local):
     vol_ms = [sum(lg.kernel_ms("rbf_eval")) for lg in logs if lg.kernel_ms("rbf_eval")]
     launches = sum(lg.count for lg in logs) / len(logs)
     launches_sel = sum(lg.by_name.get("rbf_gcb_run", 0) for lg in logs) / len(logs)
-    traffic = load_traffic()
+    traffic = {k: v.get("bytes_per_launch") for k, v in load_traffic().items()}
     peak_tf = peak["peak_tflops"]
     kernels = []
     if sel_ms:
@@ -399,7 +399,10 @@ def run_ours(args, rank, world, local):
         if dominant:
             roof = {"bound": "fp64", "achieved": dominant["achieved"], "peak": peak_tf,
                     "unit": "TFLOP/s", "frac": dominant["frac"], "traffic": dominant["traffic"],
-                    "kernel": dominant["kernel"], "peak_source": peak["source"]}
+                    "traffic_source": "profiles/ncu_traffic.json (ncu --set full, per launch)",
+                    "kernel": dominant["kernel"], "peak_source": peak["source"],
+                    "note": "the selection loop is latency bound (dependent DSMEM hops between "
+                            "phases, DESIGN.md 4.2); the volume kernel's roofline is in kernels[]"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_total / args.steps * 1e3,
