@@ -280,57 +280,64 @@ struct GlobalPath {
     __syncthreads();
   }
 
-  // errors of `card` rows; the team's CTAs split the rows, S lanes share a row
-  __device__ void scan(const int* gpos, const double* gpt, const double* gdisp, int card, int n,
-                       int par) {
+  // errors of `card` rows. The team's CTAs split the rows; a CTA takes its
+  // rows in rounds, one row per S lanes (S lanes split the supports and
+  // combine with a butterfly). Full rounds use S = 1 (512 rows); the last
+  // round spreads its remaining rows over all 16 warps (largest power-of-two
+  // S with rows * S <= 512), so a small remainder costs n/S pair steps
+  // instead of a whole round. Each row's epilogue (position, eligibility,
+  // displacement loads, residual) runs on its own lane, in parallel.
+  __device__ __forceinline__ void scan(const int* gpos, const double* gpt, const double* gdisp, int card,
+                                       int n, int par) {
     const int tid = threadIdx.x, G = gridDim.x;
     const int lo = (int)((int64_t)card * blockIdx.x / G);
     const int hi = (int)((int64_t)card * (blockIdx.x + 1) / G);
-    const int mine = hi - lo;
-    int S = 32;
-    while (S > 1 && mine * S > kLoopThreads) S >>= 1;
-    while (S > 1 && (S >> 1) >= n) S >>= 1;
-    const int groups = kLoopThreads / S;
-    const int g = tid / S, sub = tid % S;
-    const int rounds = (mine + groups - 1) / groups;
     const double* gx = a.sup;
     const int cap = a.cap;
     Best bu{-1.0, kNone}, br{-1.0, kNone};
-    for (int rd = 0; rd < rounds; ++rd) {
-      const int t = lo + rd * groups + g;
-      const bool active = t < hi;
+    bool staged = false;
+    for (int t0 = lo; t0 < hi;) {
+      const int rem = hi - t0;
+      int S = 32;
+      while (S > 1 && rem * S > kLoopThreads) S >>= 1;
+      while (S > 1 && (S >> 1) >= n) S >>= 1;
+      const int groups = kLoopThreads / S;
+      const int rows = min(rem, groups);
+      const int g = tid / S, sub = tid % S;
+      const int t = t0 + g;
+      const bool active = g < rows;
       int pos = 0;
       double px = 0.0, py = 0.0, pz = 0.0;
-      bool elig = false;
       if (active) {
         pos = gpos ? __ldg(gpos + t) : t;
         px = __ldcg(gpt + 3 * (int64_t)t) * inv_r;
         py = __ldcg(gpt + 3 * (int64_t)t + 1) * inv_r;
         pz = __ldcg(gpt + 3 * (int64_t)t + 2) * inv_r;
-        elig = !__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + pos);
       }
       double ax = 0.0, ay = 0.0, az = 0.0;
-      for (int t0 = 0; t0 < n; t0 += kSupTile) {
-        const int cnt = min(kSupTile, n - t0);
-        if (rd == 0 || n > kSupTile) {
+      for (int s0 = 0; s0 < n; s0 += kSupTile) {
+        const int cnt = min(kSupTile, n - s0);
+        if (!staged || n > kSupTile) {
           __syncthreads();
           for (int j = tid; j < cnt; j += kLoopThreads) {
-            sh.sx[j] = __ldcg(gx + t0 + j) * inv_r;
-            sh.sy[j] = __ldcg(gx + cap + t0 + j) * inv_r;
-            sh.sz[j] = __ldcg(gx + 2 * cap + t0 + j) * inv_r;
-            sh.wx[j] = __ldcg(gx + 3 * cap + t0 + j);
-            sh.wy[j] = __ldcg(gx + 4 * cap + t0 + j);
-            sh.wz[j] = __ldcg(gx + 5 * cap + t0 + j);
+            sh.sx[j] = __ldcg(gx + s0 + j) * inv_r;
+            sh.sy[j] = __ldcg(gx + cap + s0 + j) * inv_r;
+            sh.sz[j] = __ldcg(gx + 2 * cap + s0 + j) * inv_r;
+            sh.wx[j] = __ldcg(gx + 3 * cap + s0 + j);
+            sh.wy[j] = __ldcg(gx + 4 * cap + s0 + j);
+            sh.wz[j] = __ldcg(gx + 5 * cap + s0 + j);
           }
           __syncthreads();
+          staged = true;
         }
         if (active) {
 #pragma unroll 4
           for (int j = sub; j < cnt; j += S)
-            pair_accum(px, py, pz, sh.sx[j], sh.sy[j], sh.sz[j], sh.wx[j], sh.wy[j], sh.wz[j], ax,
-                       ay, az);
+            pair_accum(px, py, pz, sh.sx[j], sh.sy[j], sh.sz[j], sh.wx[j], sh.wy[j], sh.wz[j], ax, ay,
+                       az);
         }
       }
+      if (t0 == lo) pc.mark(11);
       for (int off = S >> 1; off > 0; off >>= 1) {
         ax += __shfl_xor_sync(0xffffffffu, ax, off);
         ay += __shfl_xor_sync(0xffffffffu, ay, off);
@@ -341,11 +348,15 @@ struct GlobalPath {
                                        __ldcg(gdisp + 3 * (int64_t)t + 2), ax, ay, az);
         s.err[t] = e;
         if (better(e, pos, bu.err, bu.pos)) bu = Best{e, pos};
-        if (elig && better(e, pos, br.err, br.pos)) br = Best{e, pos};
+        if (!__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + pos) && better(e, pos, br.err, br.pos))
+          br = Best{e, pos};
       }
+      t0 += rows;
     }
+    pc.mark(13);
     publish(cta_best(sh.cm, bu, 0), 0, par);
     publish(cta_best(sh.cm, br, 1), 1, par);
+    pc.mark(14);
   }
 
   __device__ int append(int pos, int& n, bool check_dup, double* pivot2_out) {
@@ -623,7 +634,7 @@ struct SmemPath {
     __syncthreads();
   }
 
-  __device__ void scan(const int* gpos, const double* gpt, const double* gdisp, int card, int n,
+  __device__ __forceinline__ void scan(const int* gpos, const double* gpt, const double* gdisp, int card, int n,
                        int par) {
     const int tid = threadIdx.x, lane = tid & 31;
     const int lo = (int)((int64_t)card * blockIdx.x / kClusterCTAs);
@@ -1163,7 +1174,7 @@ struct MsgPath {
 
   // -------------------------------------------------------------------- scan
   // targets per lane chosen so the CTA's rows fill as many warps as possible
-  __device__ void scan(const int* gpos, const double* gpt, const double* gdisp, int card, int n,
+  __device__ __forceinline__ void scan(const int* gpos, const double* gpt, const double* gdisp, int card, int n,
                        int par) {
     const int lo = (int)((int64_t)card * blockIdx.x / gridDim.x);
     const int hi = (int)((int64_t)card * (blockIdx.x + 1) / gridDim.x);
@@ -1179,7 +1190,7 @@ struct MsgPath {
   }
 
   template <int kTPT>
-  __device__ void scan_t(const int* gpos, const double* gpt, const double* gdisp, int lo, int hi, int n,
+  __device__ __forceinline__ void scan_t(const int* gpos, const double* gpt, const double* gdisp, int lo, int hi, int n,
                          int par) {
     const int tid = threadIdx.x, lane = tid & 31;
     const int tgroups = (hi - lo + kTPT - 1) / kTPT;
