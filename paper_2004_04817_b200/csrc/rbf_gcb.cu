@@ -66,6 +66,7 @@ struct LoopScratch {
   double* gdisp;   // [nb][3] displacements in group order
   double* xc;      // [2 parities][16 clusters][4]: per-cluster (err, pos) x 2
   unsigned* xseq;  // [2][16] publication sequence numbers
+  double* lic;     // [cap(cap+1)/2] column-packed copy of Li (L2 paths)
 };
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
@@ -93,6 +94,7 @@ static LoopScratch carve(void* base, int nb, int cap, int ctas, size_t* total) {
   s.gdisp = reinterpret_cast<double*>(take(sizeof(double) * 3 * (size_t)nb));
   s.xc = reinterpret_cast<double*>(take(sizeof(double) * 2 * 16 * 4));
   s.xseq = reinterpret_cast<unsigned*>(take(sizeof(unsigned) * 2 * 16));
+  s.lic = reinterpret_cast<double*>(take(sizeof(double) * (size_t)cap * (cap + 1) / 2));
   if (total) *total = off;
   return s;
 }
@@ -112,12 +114,17 @@ struct GridTeam {
   __device__ __forceinline__ void sync() const {
     __syncthreads();
     if (threadIdx.x == 0) {
+      // arrive with release semantics (cumulative over the CTA's writes via
+      // the __syncthreads above), spin with acquire loads; the short sleep
+      // keeps 148 pollers off the barrier line (tools/gridbar_bench.cu:
+      // ~2260 cycles per barrier vs ~2720 for fence + relaxed atomic)
       const unsigned add = blockIdx.x == 0 ? (0x80000000u - (gridDim.x - 1)) : 1u;
-      __threadfence();
-      const unsigned old = atomicAdd(word, add);
+      unsigned old;
+      asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(word), "r"(add) : "memory");
       uint64_t t0 = 0;
       unsigned spins = 0;
       while (((old ^ ld_acquire(word)) & 0x80000000u) == 0) {
+        __nanosleep(32);
         if ((++spins & 1023u) == 0) {
           const uint64_t now = globaltimer_ns();
           if (t0 == 0) {
@@ -188,19 +195,22 @@ __device__ __forceinline__ Best cta_best(Common& cm, Best b, int slot) {
 
 // Warp-cooperative dot product of packed row `arow` (len entries) with x,
 // every load of the lane issued before the first FMA (8 in flight per lane).
-template <typename XL>
+// kB loads of the row per lane are in flight before the first FMA; every
+// lane accumulates its entries in increasing j whatever kB is, so the result
+// does not depend on kB.
+template <int kB = 8, typename XL>
 __device__ __forceinline__ double row_dot(const double* arow, int len, XL xload, int lane) {
   double acc = 0.0;
-  for (int j0 = 0; j0 < len; j0 += 8 * kWarp) {
-    double av[8], xv[8];
+  for (int j0 = 0; j0 < len; j0 += kB * kWarp) {
+    double av[kB], xv[kB];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < kB; ++u) {
       const int j = j0 + u * kWarp + lane;
       av[u] = j < len ? __ldcg(arow + j) : 0.0;
       xv[u] = j < len ? xload(j) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc = fma(av[u], xv[u], acc);
+    for (int u = 0; u < kB; ++u) acc = fma(av[u], xv[u], acc);
   }
   return warp_sum(acc);
 }
@@ -230,6 +240,10 @@ __device__ __forceinline__ bool exact_row(Common& cm, double* row, int n, double
 }
 
 // ================================================================ GlobalPath
+// column j of a column-packed lower triangle with capacity cap: entries
+// i = j .. cap-1 contiguous from here
+__device__ __forceinline__ int64_t col_off(int64_t j, int64_t cap) { return j * cap - j * (j - 1) / 2; }
+
 struct GlobalShared {
   Common cm;
   double sx[kSupTile], sy[kSupTile], sz[kSupTile];
@@ -249,7 +263,19 @@ struct GlobalPath {
   static constexpr int kMaxN = kRowSmemMax;
   __device__ Common& cm() { return sh.cm; }
   __device__ void sync() { team.sync(); }
-  __device__ void begin(int /*n*/) {}
+  // rebuild the column-packed copy of Li (rows < n) for this launch's capacity
+  __device__ void begin(int n) {
+    const int64_t total = (int64_t)n * (n + 1) / 2;
+    const int64_t cap = a.cap;
+    for (int64_t f = (int64_t)blockIdx.x * kLoopThreads + threadIdx.x; f < total;
+         f += (int64_t)gridDim.x * kLoopThreads) {
+      int64_t i = (int64_t)((sqrt(8.0 * (double)f + 1.0) - 1.0) * 0.5);
+      while (tri_off(i + 1) <= f) ++i;
+      while (tri_off(i) > f) --i;
+      const int64_t j = f - tri_off(i);
+      s.lic[col_off(j, cap) + (i - j)] = __ldcg(a.Li + f);
+    }
+  }
   __device__ int group_off(int g) { return __ldg(a.group_off + g); }
 
   // this CTA's partial -> global, double-buffered by parity
@@ -281,35 +307,88 @@ struct GlobalPath {
   }
 
   // errors of `card` rows. The team's CTAs split the rows; a CTA takes its
-  // rows in rounds, one row per S lanes (S lanes split the supports and
-  // combine with a butterfly). Full rounds use S = 1 (512 rows); the last
-  // round spreads its remaining rows over all 16 warps (largest power-of-two
-  // S with rows * S <= 512), so a small remainder costs n/S pair steps
-  // instead of a whole round. Each row's epilogue (position, eligibility,
-  // displacement loads, residual) runs on its own lane, in parallel.
+  // rows in rounds. Full rounds give each of the 512 lanes one row. The last
+  // round (rem < 512 rows) spreads its rows over the warps: S lanes per row
+  // (the largest power of two <= 32 with rem * S <= 512), each lane
+  // accumulating supports j = sub (mod S), combined by a butterfly. Each
+  // row's position, eligibility and displacement are prefetched into shared
+  // memory before the pair loop, so the epilogues never wait on a global
+  // load. (An arbitrary S with shared-memory partials filling all 512 lanes
+  // measured slower: tools/greedy_ab.py, configs[3].)
   __device__ __forceinline__ void scan(const int* gpos, const double* gpt, const double* gdisp, int card,
                                        int n, int par) {
-    const int tid = threadIdx.x, G = gridDim.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, G = gridDim.x;
     const int lo = (int)((int64_t)card * blockIdx.x / G);
     const int hi = (int)((int64_t)card * (blockIdx.x + 1) / G);
     const double* gx = a.sup;
     const int cap = a.cap;
+    // tail-round operands in the (idle) row buffer
+    double* md = sh.row;                                            // [kLoopThreads][3] displacements
+    int* mpos = reinterpret_cast<int*>(sh.row + 3 * kLoopThreads);  // [kLoopThreads] pos (~pos: ineligible)
     Best bu{-1.0, kNone}, br{-1.0, kNone};
     bool staged = false;
+    auto stage = [&](int s0, int cnt) {
+      __syncthreads();
+      for (int j = tid; j < cnt; j += kLoopThreads) {
+        sh.sx[j] = __ldcg(gx + s0 + j) * inv_r;
+        sh.sy[j] = __ldcg(gx + cap + s0 + j) * inv_r;
+        sh.sz[j] = __ldcg(gx + 2 * cap + s0 + j) * inv_r;
+        sh.wx[j] = __ldcg(gx + 3 * cap + s0 + j);
+        sh.wy[j] = __ldcg(gx + 4 * cap + s0 + j);
+        sh.wz[j] = __ldcg(gx + 5 * cap + s0 + j);
+      }
+      __syncthreads();
+    };
+    auto finish_row = [&](int t, int pos, bool elig, double dx, double dy, double dz, double ux, double uy,
+                          double uz) {
+      const double e = residual_norm(dx, dy, dz, ux, uy, uz);
+      s.err[t] = e;
+      if (better(e, pos, bu.err, bu.pos)) bu = Best{e, pos};
+      if (elig && better(e, pos, br.err, br.pos)) br = Best{e, pos};
+    };
     for (int t0 = lo; t0 < hi;) {
       const int rem = hi - t0;
+      if (rem >= kLoopThreads) {  // full round: one row per lane
+        const int t = t0 + tid;
+        const int pos = gpos ? __ldg(gpos + t) : t;
+        const double px = __ldcg(gpt + 3 * (int64_t)t) * inv_r, py = __ldcg(gpt + 3 * (int64_t)t + 1) * inv_r,
+                     pz = __ldcg(gpt + 3 * (int64_t)t + 2) * inv_r;
+        double ax = 0.0, ay = 0.0, az = 0.0;
+        for (int s0 = 0; s0 < n; s0 += kSupTile) {
+          const int cnt = min(kSupTile, n - s0);
+          if (!staged || n > kSupTile) {
+            stage(s0, cnt);
+            staged = true;
+          }
+#pragma unroll 4
+          for (int j = 0; j < cnt; ++j)
+            pair_accum(px, py, pz, sh.sx[j], sh.sy[j], sh.sz[j], sh.wx[j], sh.wy[j], sh.wz[j], ax, ay, az);
+        }
+        if (t0 == lo) pc.mark(11);
+        finish_row(t, pos, !__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + pos),
+                   __ldcg(gdisp + 3 * (int64_t)t), __ldcg(gdisp + 3 * (int64_t)t + 1),
+                   __ldcg(gdisp + 3 * (int64_t)t + 2), ax, ay, az);
+        t0 += kLoopThreads;
+        continue;
+      }
+      // tail round: rem rows, S = a power of two <= 32 lanes per row
       int S = 32;
       while (S > 1 && rem * S > kLoopThreads) S >>= 1;
       while (S > 1 && (S >> 1) >= n) S >>= 1;
-      const int groups = kLoopThreads / S;
-      const int rows = min(rem, groups);
       const int g = tid / S, sub = tid % S;
+      const bool active = g < rem;
       const int t = t0 + g;
-      const bool active = g < rows;
-      int pos = 0;
+      if (tid < rem) {  // prefetch row tid's epilogue operands
+        const int tt = t0 + tid;
+        const int pos = gpos ? __ldg(gpos + tt) : tt;
+        const bool elig = !__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + pos);
+        mpos[tid] = elig ? pos : ~pos;
+        md[3 * tid] = __ldcg(gdisp + 3 * (int64_t)tt);
+        md[3 * tid + 1] = __ldcg(gdisp + 3 * (int64_t)tt + 1);
+        md[3 * tid + 2] = __ldcg(gdisp + 3 * (int64_t)tt + 2);
+      }
       double px = 0.0, py = 0.0, pz = 0.0;
       if (active) {
-        pos = gpos ? __ldg(gpos + t) : t;
         px = __ldcg(gpt + 3 * (int64_t)t) * inv_r;
         py = __ldcg(gpt + 3 * (int64_t)t + 1) * inv_r;
         pz = __ldcg(gpt + 3 * (int64_t)t + 2) * inv_r;
@@ -318,23 +397,13 @@ struct GlobalPath {
       for (int s0 = 0; s0 < n; s0 += kSupTile) {
         const int cnt = min(kSupTile, n - s0);
         if (!staged || n > kSupTile) {
-          __syncthreads();
-          for (int j = tid; j < cnt; j += kLoopThreads) {
-            sh.sx[j] = __ldcg(gx + s0 + j) * inv_r;
-            sh.sy[j] = __ldcg(gx + cap + s0 + j) * inv_r;
-            sh.sz[j] = __ldcg(gx + 2 * cap + s0 + j) * inv_r;
-            sh.wx[j] = __ldcg(gx + 3 * cap + s0 + j);
-            sh.wy[j] = __ldcg(gx + 4 * cap + s0 + j);
-            sh.wz[j] = __ldcg(gx + 5 * cap + s0 + j);
-          }
-          __syncthreads();
+          stage(s0, cnt);
           staged = true;
         }
         if (active) {
 #pragma unroll 4
           for (int j = sub; j < cnt; j += S)
-            pair_accum(px, py, pz, sh.sx[j], sh.sy[j], sh.sz[j], sh.wx[j], sh.wy[j], sh.wz[j], ax, ay,
-                       az);
+            pair_accum(px, py, pz, sh.sx[j], sh.sy[j], sh.sz[j], sh.wx[j], sh.wy[j], sh.wz[j], ax, ay, az);
         }
       }
       if (t0 == lo) pc.mark(11);
@@ -343,20 +412,48 @@ struct GlobalPath {
         ay += __shfl_xor_sync(0xffffffffu, ay, off);
         az += __shfl_xor_sync(0xffffffffu, az, off);
       }
+      __syncthreads();  // prefetched operands visible
       if (active && sub == 0) {
-        const double e = residual_norm(__ldcg(gdisp + 3 * (int64_t)t), __ldcg(gdisp + 3 * (int64_t)t + 1),
-                                       __ldcg(gdisp + 3 * (int64_t)t + 2), ax, ay, az);
-        s.err[t] = e;
-        if (better(e, pos, bu.err, bu.pos)) bu = Best{e, pos};
-        if (!__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + pos) && better(e, pos, br.err, br.pos))
-          br = Best{e, pos};
+        const int mp = mpos[g];
+        const bool elig = mp >= 0;
+        finish_row(t, elig ? mp : ~mp, elig, md[3 * g], md[3 * g + 1], md[3 * g + 2], ax, ay, az);
       }
-      t0 += rows;
+      __syncthreads();
+      t0 += rem;
     }
     pc.mark(13);
     publish(cta_best(sh.cm, bu, 0), 0, par);
     publish(cta_best(sh.cm, br, 1), 1, par);
     pc.mark(14);
+  }
+
+  // Products with the n vectors of a packed triangle: rows of a row-packed
+  // triangle (vector i, length i + 1) or, with kCols, columns of the
+  // column-packed copy (vector j = rows j..n-1, x index j + e); one warp per
+  // vector, vectors strided over every warp of the team, 16 loads per lane
+  // in flight once the factor is long. finish(v, sum) runs on lane 0.
+  template <bool kCols, class XL, class Fin>
+  __device__ __forceinline__ void tri_gemv(const double* A, int n, XL xload, Fin finish) {
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * kLoopWarps + (threadIdx.x >> 5), nw = gridDim.x * kLoopWarps;
+    const int64_t cap = a.cap;
+    for (int v = gw; v < n; v += nw) {
+      const double* av = A + (kCols ? col_off(v, cap) : tri_off(v));
+      const int len = kCols ? n - v : v + 1;
+      auto xl = [&](int e) { return xload(v, e); };
+      const double acc = len > 1024 ? row_dot<16>(av, len, xl, lane) : row_dot<8>(av, len, xl, lane);
+      if (lane == 0) finish(v, acc);
+    }
+  }
+
+  // x (n doubles) into shared memory (the scan's staging area is idle
+  // during an append) once it is long enough for the copy to pay
+  __device__ __forceinline__ const double* stage_x(const double* x, int n) {
+    if (n <= 1024) return nullptr;
+    double* xs = sh.sx;  // sx..wz: 6 * kSupTile contiguous doubles >= kRowSmemMax
+    for (int j = threadIdx.x; j < n; j += kLoopThreads) xs[j] = __ldcg(x + j);
+    __syncthreads();
+    return xs;
   }
 
   __device__ int append(int pos, int& n, bool check_dup, double* pivot2_out) {
@@ -373,31 +470,29 @@ struct GlobalPath {
     });
     if (check_dup && n > 0 && near) return kRejectDup;
     pc.mark(1);
-    const int gw = blockIdx.x * kLoopWarps + warp, nw = G * kLoopWarps;
-    for (int i = gw; i < n; i += nw) {  // c0 = Li row
-      const double v = row_dot(a.Li + tri_off(i), i + 1, [&](int j) { return row[j]; }, lane);
-      if (lane == 0) s.c0[i] = v;
-    }
+    // c0 = Li row
+    tri_gemv<false>(a.Li, n, [&](int, int e) { return row[e]; },
+                    [&](int v, double acc) { s.c0[v] = acc; });
     team.sync();
     pc.mark(2);
-    for (int i = gw; i < n; i += nw) {  // r = row - L c0
-      const double v = row_dot(a.L + tri_off(i), i + 1, [&](int j) { return __ldcg(s.c0 + j); }, lane);
-      if (lane == 0) s.r[i] = row[i] - v;
-    }
+    // r = row - L c0
+    const double* xs = stage_x(s.c0, n);
+    tri_gemv<false>(a.L, n, [&](int, int e) { return xs ? xs[e] : __ldcg(s.c0 + e); },
+                    [&](int v, double acc) { s.r[v] = row[v] - acc; });
     team.sync();
     pc.mark(3);
+    // c = c0 + Li r, with this CTA's partials of c.c and c.y
     double pcc = 0.0, pcy0 = 0.0, pcy1 = 0.0, pcy2 = 0.0;
-    for (int i = gw; i < n; i += nw) {  // c = c0 + Li r
-      const double v = row_dot(a.Li + tri_off(i), i + 1, [&](int j) { return __ldcg(s.r + j); }, lane);
-      if (lane == 0) {
-        const double c = __ldcg(s.c0 + i) + v;
-        s.c1[i] = c;
-        pcc = fma(c, c, pcc);
-        pcy0 = fma(c, __ldcg(a.y + 3 * (int64_t)i), pcy0);
-        pcy1 = fma(c, __ldcg(a.y + 3 * (int64_t)i + 1), pcy1);
-        pcy2 = fma(c, __ldcg(a.y + 3 * (int64_t)i + 2), pcy2);
-      }
-    }
+    __syncthreads();
+    xs = stage_x(s.r, n);
+    tri_gemv<false>(a.Li, n, [&](int, int e) { return xs ? xs[e] : __ldcg(s.r + e); }, [&](int v, double acc) {
+      const double c = __ldcg(s.c0 + v) + acc;
+      s.c1[v] = c;
+      pcc = fma(c, c, pcc);
+      pcy0 = fma(c, __ldcg(a.y + 3 * (int64_t)v), pcy0);
+      pcy1 = fma(c, __ldcg(a.y + 3 * (int64_t)v + 1), pcy1);
+      pcy2 = fma(c, __ldcg(a.y + 3 * (int64_t)v + 2), pcy2);
+    });
     Common& cm = sh.cm;
     if (lane == 0) {
       cm.wred[warp][0] = pcc;
@@ -438,19 +533,22 @@ struct GlobalPath {
     double* Lrow = a.L + tri_off(n);
     double* Lirow = a.Li + tri_off(n);
     double* wgt = a.sup + 3 * (int64_t)cap;
-    tri_cols<4, kLoopWarps>(
-        a.Li, n,
-        [&](int i, int c) { return c == 0 ? __ldcg(s.c1 + i) : __ldcg(a.y + 3 * (int64_t)i + (c - 1)); },
-        (int)blockIdx.x, G, cm.red, [&](int j, const double* sum) {
-          const double lij = -sum[0] / l;
-          Lirow[j] = lij;
-          Lrow[j] = __ldcg(s.c1 + j);
-          wgt[j] = fma(lij, yn0, sum[1]);
-          wgt[cap + j] = fma(lij, yn1, sum[2]);
-          wgt[2 * cap + j] = fma(lij, yn2, sum[3]);
-        });
+    // u = Li^T c over the column copy; Li[n][j] = -u_j / l, and the weights
+    // move by Li[n][j] y_n (w = Li^T y with the new row appended)
+    const int nn = n;
+    xs = stage_x(s.c1, n);
+    tri_gemv<true>(s.lic, n, [&](int v, int e) { return xs ? xs[v + e] : __ldcg(s.c1 + v + e); }, [&](int j, double u) {
+      const double lij = -u / l;
+      Lirow[j] = lij;
+      s.lic[col_off(j, cap) + (nn - j)] = lij;
+      Lrow[j] = __ldcg(s.c1 + j);
+      wgt[j] = fma(lij, yn0, __ldcg(wgt + j));
+      wgt[cap + j] = fma(lij, yn1, __ldcg(wgt + cap + j));
+      wgt[2 * cap + j] = fma(lij, yn2, __ldcg(wgt + 2 * cap + j));
+    });
     if (blockIdx.x == 0 && tid == 0) {
       Lirow[n] = 1.0 / l;
+      s.lic[col_off(n, cap)] = 1.0 / l;
       Lrow[n] = l;
       a.y[3 * (int64_t)n] = yn0;
       a.y[3 * (int64_t)n + 1] = yn1;
@@ -984,6 +1082,7 @@ struct MsgShared {
 static_assert(sizeof(MsgShared) <= 227 * 1024, "MsgShared exceeds shared memory");
 static_assert(sizeof(SmemShared) <= 227 * 1024, "SmemShared exceeds shared memory");
 static_assert(sizeof(GlobalShared) <= 227 * 1024, "GlobalShared exceeds shared memory");
+static_assert(6 * kSupTile >= kRowSmemMax, "stage_x uses sx..wz as one kRowSmemMax buffer");
 
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
