@@ -89,6 +89,18 @@ RBF_API int rbf_errors_argmax(const double* bnd_points, const double* bnd_disp,
                       void* scratch, size_t scratch_bytes, void* stream);
 
 /* ---------------------------------------------------------------------
+ * Nearest-support distances.  Replaces metrics.py:45-48
+ * `_nearest_distances` (cdist + row min, used by kl_divergence
+ * metrics.py:63-74) and metrics.py:51-60 `nearest_support_distance`:
+ *   out[k] = min_i | t_k - s_i |_2
+ * with cdist's rounding, sqrt((dx*dx + dy*dy) + dz*dz) uncontracted, so the
+ * distances are bit-identical to the reference's. Device pointers, AoS
+ * (n,3) float64; n_sup = 0 -> RBF_EARG ("support set is empty").
+ */
+RBF_API int rbf_nearest(const double* targets, int64_t n_targets,
+                const double* sup_points, int64_t n_sup, double* out, void* stream);
+
+/* ---------------------------------------------------------------------
  * Growing Cholesky factor.  Replaces core.py:115-205 `CholeskyState`.
  * The factor L and its inverse Li are stored as PACKED lower triangles,
  * row-major (row i starts at i*(i+1)/2), so capacity growth is a prefix

@@ -265,6 +265,51 @@ def select(pts, disp, radius, tol, max_supports, m=1, seed=0, threads=1, ids=Non
     }
 
 
+# ------------------------------------------------------------------ metrics
+KL_FLOOR = 1e-12  # reference metrics.py:14-16
+
+
+def nearest_distances(pts, sup_pts):
+    """min over supports of cdist (reference metrics.py:45-48)."""
+    return cdist(pts, sup_pts).min(axis=1)
+
+
+def kl_divergence(pts, sup1, sup2):
+    """reference metrics.py:63-74"""
+    d1 = nearest_distances(pts, sup1)
+    d2 = np.maximum(nearest_distances(pts, sup2), KL_FLOOR)
+    mask = d1 > 0.0
+    return float(np.sum(d1[mask] * np.log(d1[mask] / d2[mask])))
+
+
+def error_summary(pts, disp, ids, sup_pts, sup_w, radius):
+    """(max, rms, id of max) over all boundary rows (reference metrics.py:77-88)."""
+    errors = residual_errors(np.arange(len(pts)), pts, disp, sup_pts, sup_w, radius)
+    worst = argmax_low(errors, ids)
+    return float(errors[worst]), float(np.sqrt(np.mean(errors * errors))), int(ids[worst])
+
+
+def error_history(pts, disp, ids, support_ids, radius, every=50):
+    """Per-prefix summaries with a one-shot Cholesky per prefix
+    (reference metrics.py:91-115)."""
+    from scipy.linalg import cho_factor, cho_solve
+
+    support_ids = np.asarray(support_ids, dtype=np.intp)
+    total = len(support_ids)
+    counts = list(range(every, total, every))
+    if not counts or counts[-1] != total:
+        counts.append(total)
+    positions = np.searchsorted(ids, support_ids)
+    out = []
+    with threadpool_limits(1):
+        for n in counts:
+            p = pts[positions[:n]]
+            a = phi(cdist(p, p) / radius)
+            w = cho_solve(cho_factor(a, lower=True), disp[positions[:n]])
+            out.append((n, error_summary(pts, disp, ids, p, w, radius)))
+    return out
+
+
 def default_threads():
     try:
         return len(os.sched_getaffinity(0))

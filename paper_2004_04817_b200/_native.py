@@ -119,6 +119,7 @@ SIGNATURES = [
     ("rbf_errors_argmax", ctypes.c_int,
      [c_dp, c_dp, c_dp, ctypes.c_int64, c_dp, c_dp, ctypes.c_int64, ctypes.c_double, c_dp,
       ctypes.POINTER(ctypes.c_double), c_dp, ctypes.c_size_t, c_dp]),
+    ("rbf_nearest", ctypes.c_int, [c_dp, ctypes.c_int64, c_dp, ctypes.c_int64, c_dp, c_dp]),
     ("rbf_chol_scratch_bytes", ctypes.c_size_t, [ctypes.c_int64]),
     ("rbf_chol_append", ctypes.c_int,
      [c_dp, c_dp, ctypes.c_int64, c_dp, ctypes.POINTER(ctypes.c_double), c_dp, ctypes.c_size_t, c_dp]),

@@ -190,17 +190,25 @@ class CholeskyState:
             raise DimensionMismatchError(
                 f"rhs has leading dimension {rhs.shape[:1]}, factor order is {self._n}"
             )
-        if self._n == 0:
+        return self._solve_prefix(rhs, self._n)
+
+    def _solve_prefix(self, rhs, n):
+        """Solve with the leading order-n block of the factor (the factor of
+        the first n appended rows; a prefix of the packed triangles)."""
+        rhs = np.asarray(rhs, dtype=float)
+        if not 0 <= n <= self._n or rhs.shape[:1] != (n,):
+            raise DimensionMismatchError(f"prefix {n} / rhs {rhs.shape} vs factor order {self._n}")
+        if n == 0:
             return rhs.copy()
         lib = N.require_cuda()
         t = N.torch()
         k = 1 if rhs.ndim == 1 else int(np.prod(rhs.shape[1:]))
-        b = _to_device(rhs.reshape(self._n, k))
+        b = _to_device(rhs.reshape(n, k))
         out = t.empty_like(b)
-        nbytes = 3 * self._n * k * 8
+        nbytes = 3 * n * k * 8
         scratch = t.empty(nbytes, dtype=t.uint8, device=_device())
         with N.launching("rbf_chol_solve", kernels=6 * ((k + 3) // 4)):
-            rc = lib.rbf_chol_solve(N.dptr(self._L), N.dptr(self._Li), self._n, N.dptr(b), k,
+            rc = lib.rbf_chol_solve(N.dptr(self._L), N.dptr(self._Li), n, N.dptr(b), k,
                                     N.dptr(out), N.dptr(scratch), nbytes, N.stream_ptr())
         N.check(rc, "rbf_chol_solve")
         return _to_host(out).reshape(rhs.shape)

@@ -297,3 +297,68 @@ extern "C" int rbf_errors_argmax(const double* bnd_points, const double* bnd_dis
   }
   return RBF_OK;
 }
+
+// ------------------------------------------------------------ nearest support
+// out[k] = min_i |t_k - s_i|_2 with scipy cdist's rounding (reference
+// metrics.py:45-48 `_nearest_distances`, metrics.py:51-60
+// `nearest_support_distance`): squared distance (dx*dx + dy*dy) + dz*dz
+// without contraction, the minimum over supports, one correctly rounded
+// sqrt at the end (sqrt is monotone and correctly rounded, so
+// sqrt(min d^2) == min sqrt(d^2) bit for bit). Coordinates are not scaled.
+constexpr int kNearThreads = 128, kNearTPT = 4, kNearTile = 256;
+
+__global__ void __launch_bounds__(kNearThreads)
+nearest_kernel(const double* __restrict__ tpts, int64_t nt, const double* __restrict__ spts, int nsup,
+               double* __restrict__ out) {
+  __shared__ double s_x[kNearTile], s_y[kNearTile], s_z[kNearTile];
+  const int64_t base = (int64_t)blockIdx.x * (kNearThreads * kNearTPT) + threadIdx.x;
+  double px[kNearTPT], py[kNearTPT], pz[kNearTPT], dmin[kNearTPT];
+#pragma unroll
+  for (int k = 0; k < kNearTPT; ++k) {
+    const int64_t r = base + (int64_t)k * kNearThreads;
+    const bool ok = r < nt;
+    px[k] = ok ? tpts[3 * r] : 0.0;
+    py[k] = ok ? tpts[3 * r + 1] : 0.0;
+    pz[k] = ok ? tpts[3 * r + 2] : 0.0;
+    dmin[k] = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  }
+  for (int t0 = 0; t0 < nsup; t0 += kNearTile) {
+    const int cnt = min(kNearTile, nsup - t0);
+    __syncthreads();
+    for (int j = threadIdx.x; j < cnt; j += kNearThreads) {
+      s_x[j] = spts[3 * (int64_t)(t0 + j)];
+      s_y[j] = spts[3 * (int64_t)(t0 + j) + 1];
+      s_z[j] = spts[3 * (int64_t)(t0 + j) + 2];
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int j = 0; j < cnt; ++j) {
+      const double sx = s_x[j], sy = s_y[j], sz = s_z[j];
+#pragma unroll
+      for (int k = 0; k < kNearTPT; ++k) {
+        const double dx = __dsub_rn(px[k], sx), dy = __dsub_rn(py[k], sy), dz = __dsub_rn(pz[k], sz);
+        const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+        dmin[k] = fmin(dmin[k], d2);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kNearTPT; ++k) {
+    const int64_t r = base + (int64_t)k * kNearThreads;
+    if (r < nt) out[r] = __dsqrt_rn(dmin[k]);
+  }
+}
+
+extern "C" int rbf_nearest(const double* targets, int64_t n_targets, const double* sup_points, int64_t n_sup,
+                           double* out, void* stream) {
+  if (n_targets < 0 || n_sup < 0) return set_error(RBF_EARG, "negative size");
+  if (n_sup == 0) return set_error(RBF_EARG, "support set is empty");
+  if (n_sup > INT32_MAX) return set_error(RBF_EARG, "too many supports");
+  if (n_targets == 0) return RBF_OK;
+  if (!targets || !sup_points || !out) return set_error(RBF_EARG, "null pointer");
+  const int64_t per = (int64_t)kNearThreads * kNearTPT;
+  nearest_kernel<<<(unsigned)((n_targets + per - 1) / per), kNearThreads, 0, as_stream(stream)>>>(
+      targets, n_targets, sup_points, (int)n_sup, out);
+  RBF_LAUNCH_CHECK("nearest_kernel");
+  return RBF_OK;
+}

@@ -317,7 +317,7 @@ struct GlobalPath {
   // measured slower: tools/greedy_ab.py, configs[3].)
   __device__ __forceinline__ void scan(const int* gpos, const double* gpt, const double* gdisp, int card,
                                        int n, int par) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, G = gridDim.x;
+    const int tid = threadIdx.x, G = gridDim.x;
     const int lo = (int)((int64_t)card * blockIdx.x / G);
     const int hi = (int)((int64_t)card * (blockIdx.x + 1) / G);
     const double* gx = a.sup;

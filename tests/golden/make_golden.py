@@ -96,6 +96,8 @@ def volume_sample(wl, support, radius, n=4096):
 
 
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "metrics":  # only the metrics case
+        return metrics_only()
     # 1. explicit small inputs (stored)
     pts, disp = hemisphere()
     for m in (1, 4):
@@ -131,6 +133,25 @@ def main():
     rhs = rng.normal(size=(150, 3))
     save("chol150", points=a_pts, L=st.factor, rhs=rhs, x=st.solve(rhs), radius=np.array(3.0))
 
+    # 2b. metrics (reference metrics.py): nearest distances, KL, summaries, history
+    from rbfdeform import metrics as RM
+
+    pts, disp = smooth(3)
+    b = R.BoundarySet(indices=np.arange(len(pts)) * 3 + 1, points=pts, disp=disp)
+    res = R.gcb_select(b, R.SelectionConfig(radius=3.0, tol=1e-4, max_supports=60, m=4, seed=2))
+    rnd = R.random_select(b, 25, seed=9, radius=3.0)
+    summ = RM.error_summary(b, res.support, 3.0)
+    hist = RM.error_history(b, res.support.nodes, 3.0, every=10)
+    save("metrics_smooth3", points=pts, disp=disp, ids=b.indices, sup_nodes=res.support.nodes,
+         sup_weights=res.support.weights, rnd_nodes=rnd.nodes, rnd_weights=rnd.weights,
+         nearest=RM._nearest_distances(res.support, b), nearest_rnd=RM._nearest_distances(rnd, b),
+         kl=np.array(RM.kl_divergence(res.support, rnd, b)),
+         kl_rev=np.array(RM.kl_divergence(rnd, res.support, b)),
+         summary=np.array([summ.max_error, summ.rms_error]), summary_node=np.array(summ.node_of_max),
+         hist_n=np.array([n for n, _ in hist]), hist_max=np.array([h.max_error for _, h in hist]),
+         hist_rms=np.array([h.rms_error for _, h in hist]),
+         hist_node=np.array([h.node_of_max for _, h in hist]), radius=np.array(3.0))
+
     # 3. BASELINE configs (generator parameters + digest; outputs)
     for idx, ms in ((0, (1, 8)),):
         wl = W.config(idx, nv=100_000)
@@ -156,6 +177,13 @@ def main():
     out, res = run_selection(wl.points, wl.disp, wl.radius, wl.tol, wl.nb, 48, 0)
     vidx, u = volume_sample(wl, res.support, wl.radius)
     save("cfg2s_m48", digest=np.array(digest(wl.points, wl.disp, wl.volume)), vol_idx=vidx, vol_u=u, **out)
+
+
+def metrics_only():
+    src = open(__file__).read()
+    a = src.index("    # 2b. metrics")
+    b = src.index("    # 3. BASELINE configs")
+    exec(compile("if True:\n" + src[a:b], __file__, "exec"), globals())
 
 
 if __name__ == "__main__":

@@ -136,3 +136,23 @@ def test_oracle_matches_reference_live(seed):
         q = rng.normal(size=(3000, 3))
         assert np.array_equal(O.eval_sum(q, ref.support.points, ref.support.weights, 2.5),
                               R.evaluate_displacements(q, ref.support, 2.5))
+
+
+def test_oracle_metrics_match_reference_golden():
+    """nearest distances, KL, error summary and history (reference metrics.py)
+    restated in the oracle reproduce the reference's bits."""
+    g = load_golden("metrics_smooth3")
+    pts, disp, ids, r = g["points"], g["disp"], g["ids"], float(g["radius"])
+    pos = np.searchsorted(ids, g["sup_nodes"])
+    rpos = np.searchsorted(ids, g["rnd_nodes"])
+    assert np.array_equal(O.nearest_distances(pts, pts[pos]), g["nearest"])
+    assert np.array_equal(O.nearest_distances(pts, pts[rpos]), g["nearest_rnd"])
+    assert O.kl_divergence(pts, pts[pos], pts[rpos]) == float(g["kl"])
+    assert O.kl_divergence(pts, pts[rpos], pts[pos]) == float(g["kl_rev"])
+    mx, rms, node = O.error_summary(pts, disp, ids, pts[pos], g["sup_weights"], r)
+    assert (mx, rms) == tuple(g["summary"].tolist()) and node == int(g["summary_node"])
+    hist = O.error_history(pts, disp, ids, g["sup_nodes"], r, every=10)
+    assert [n for n, _ in hist] == g["hist_n"].tolist()
+    assert [h[0] for _, h in hist] == g["hist_max"].tolist()
+    assert [h[1] for _, h in hist] == g["hist_rms"].tolist()
+    assert [h[2] for _, h in hist] == g["hist_node"].tolist()
