@@ -14,6 +14,8 @@ scan, t2 = weights update + candidate appends (carried into the next
 record, selection.py:310-316, 357).
 """
 
+import threading
+from collections import OrderedDict
 from dataclasses import dataclass, field, replace
 
 import numpy as np
@@ -245,19 +247,53 @@ def stage_boundary(boundary):
     must not be modified afterwards; re-stage if they are)."""
     boundary._device = (boundary.points, boundary.disp, _to_device(boundary.points),
                         _to_device(boundary.disp))
-    boundary._workspace = {}  # partitions and loop buffers reused by later selections
     return boundary
 
 
-def _workspace(boundary):
-    """Per-staged-boundary cache (None when the boundary is not staged or its
-    arrays were replaced): device partitions keyed by (m, seed) and loop
-    buffers keyed by their shape, so a repeated selection skips the host
-    partition, the H2D copies and the allocations."""
-    cached = getattr(boundary, "_device", None)
-    if cached is None or cached[0] is not boundary.points or cached[1] is not boundary.disp:
-        return None
-    return getattr(boundary, "_workspace", None)
+# Reuse across selections (thread-safe): the partition depends only on
+# (nb, m, seed), so its device copy is cached; loop buffers hold no user data
+# once a selection has returned (results are host copies), so they go back to
+# a pool keyed by shape and device. A selection takes its buffers out of the
+# pool for its whole run: concurrent selections never share them.
+_cache_lock = threading.Lock()
+_part_cache = OrderedDict()  # (device, nb, m, seed) -> (off, gpos, goff)
+_PART_CACHE_MAX = 16
+_buf_pool = {}               # (device, nb, cap, rec_cap, ctas) -> [_LoopBuffers]
+
+
+def _partition_device(nb, m, seed):
+    t = N.torch()
+    key = (t.cuda.current_device(), nb, m, seed)
+    with _cache_lock:
+        hit = _part_cache.get(key)
+        if hit is not None:
+            _part_cache.move_to_end(key)
+            return hit
+    flat, off = _partition_native(nb, m, seed)
+    part = (off, _to_device(flat, dtype=t.int32), _to_device(off, dtype=t.int32))
+    with _cache_lock:
+        _part_cache[key] = part
+        while len(_part_cache) > _PART_CACHE_MAX:
+            _part_cache.popitem(last=False)
+    return part
+
+
+def _take_buffers(nb, cap, rec_cap, ctas):
+    key = (N.torch().cuda.current_device(), nb, cap, rec_cap, ctas)
+    with _cache_lock:
+        free = _buf_pool.get(key)
+        buf = free.pop() if free else None
+    if buf is None:
+        return key, _LoopBuffers(nb, cap, rec_cap, ctas)
+    buf.reset()
+    return key, buf
+
+
+def _give_buffers(key, buf):
+    with _cache_lock:
+        free = _buf_pool.setdefault(key, [])
+        if len(free) < 2:
+            free.append(buf)
 
 
 def _boundary_on_device(boundary):
@@ -477,14 +513,7 @@ def _gcb_run(boundary, config, mode=None):
     radius = float(config.radius)
     lib = N.require_cuda()
     t = N.torch()
-    ws = _workspace(boundary)
-    part = ws.get(("part", m, config.seed)) if ws is not None else None
-    if part is None:
-        flat, off = _partition_native(nb, m, config.seed)
-        part = (off, _to_device(flat, dtype=t.int32), _to_device(off, dtype=t.int32))
-        if ws is not None:
-            ws[("part", m, config.seed)] = part
-    off, gpos, goff = part
+    off, gpos, goff = _partition_device(nb, m, config.seed)
 
     ctas = N.ctypes.c_int32(0)
     resolved = N.ctypes.c_int32(0)
@@ -499,12 +528,7 @@ def _gcb_run(boundary, config, mode=None):
             "rbf_gcb_ctas")
     pts, disp = _boundary_on_device(boundary)
     cap = _initial_capacity(config, nb)
-    bkey = ("buf", cap, 2 * cap + m + 8, ctas.value)
-    buf = ws.pop(bkey, None) if ws is not None else None
-    if buf is None:
-        buf = _LoopBuffers(nb, cap, 2 * cap + m + 8, ctas.value)
-    else:
-        buf.reset()
+    bkey, buf = _take_buffers(nb, cap, 2 * cap + m + 8, ctas.value)
 
     args = N.GcbArgs()
     args.points, args.disp = pts.data_ptr(), disp.data_ptr()
@@ -564,8 +588,7 @@ def _gcb_run(boundary, config, mode=None):
     n = st.n
     nrec = st.n_records
     sel, weights, recs = buf.unpack(host, n, nrec)
-    if ws is not None:  # results are host copies: the buffers can serve the next call
-        ws[bkey] = buf  # (a scratch sized for more CTAs also serves fewer)
+    _give_buffers(bkey, buf)  # (a scratch sized for more CTAs also serves fewer)
 
     sizes = np.diff(off)
     history = SelectionHistory(seed=config.seed, m=m)
