@@ -143,10 +143,67 @@ __global__ void __launch_bounds__(kThreads, 1) seg(const double* A, const double
   }
 }
 
+// x staged in shared memory (as the selection kernel does for long rows),
+// kB loads of A per lane in flight, optional 16-byte loads
+template <int kB, bool kVec>
+__global__ void __launch_bounds__(kThreads, 1) rowwarp_sx(const double* A, const double* x, double* y, int n) {
+  extern __shared__ double xs[];
+  for (int j = threadIdx.x; j < n; j += kThreads) xs[j] = __ldcg(x + j);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kWarps + (threadIdx.x >> 5), nw = gridDim.x * kWarps;
+  for (int i = gw; i < n; i += nw) {
+    const double* a = A + tri(i);
+    const int len = i + 1;
+    double acc = 0.0;
+    if (!kVec) {
+      for (int j0 = 0; j0 < len; j0 += kB * 32) {
+        double av[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int j = j0 + u * 32 + lane;
+          av[u] = j < len ? __ldcg(a + j) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int j = j0 + u * 32 + lane;
+          acc = fma(av[u], j < len ? xs[j] : 0.0, acc);
+        }
+      }
+    } else {
+      // peel to a 16-byte boundary, then double2 per lane
+      const int head = (int)((reinterpret_cast<uintptr_t>(a) >> 3) & 1);  // 1 if a is 8 mod 16
+      if (head && lane == 0) acc = fma(__ldcg(a), xs[0], acc);
+      const double2* a2 = reinterpret_cast<const double2*>(a + head);
+      const int len2 = (len - head) >> 1;
+      for (int j0 = 0; j0 < len2; j0 += kB * 32) {
+        double2 av[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int j = j0 + u * 32 + lane;
+          av[u] = j < len2 ? __ldcg(a2 + j) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int j = j0 + u * 32 + lane;
+          if (j < len2) {
+            acc = fma(av[u].x, xs[head + 2 * j], acc);
+            acc = fma(av[u].y, xs[head + 2 * j + 1], acc);
+          }
+        }
+      }
+      const int tail = head + 2 * len2;
+      if (tail < len && lane == 0) acc = fma(__ldcg(a + tail), xs[tail], acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) y[i] = acc;
+  }
+}
+
 int main() {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  for (int n : {427, 854, 2200, 4379, 6400}) {
+  for (int n : {854, 2200, 4379, 6400}) {
     const int64_t T = tri(n);
     std::vector<double> hA(T), hx(n);
     for (int64_t f = 0; f < T; ++f) hA[f] = 1.0 / (1 + (f % 97));
@@ -184,6 +241,15 @@ int main() {
       time("rowwarp16", [&] { rowwarp<16><<<sms, kThreads>>>(A, x, y, n); }, cold);
       time("rowbal", [&] { rowbal<<<sms, kThreads>>>(A, x, y, n); }, cold);
       time("seg", [&] { seg<<<sms, kThreads>>>(A, x, y, n); }, cold);
+      const size_t sm = 8 * (size_t)n;
+      cudaFuncSetAttribute(rowwarp_sx<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+      cudaFuncSetAttribute(rowwarp_sx<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+      cudaFuncSetAttribute(rowwarp_sx<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+      cudaFuncSetAttribute(rowwarp_sx<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+      time("sx16", [&] { rowwarp_sx<16, false><<<sms, kThreads, sm>>>(A, x, y, n); }, cold);
+      time("sx32", [&] { rowwarp_sx<32, false><<<sms, kThreads, sm>>>(A, x, y, n); }, cold);
+      time("sx_v8", [&] { rowwarp_sx<8, true><<<sms, kThreads, sm>>>(A, x, y, n); }, cold);
+      time("sx_v16", [&] { rowwarp_sx<16, true><<<sms, kThreads, sm>>>(A, x, y, n); }, cold);
     }
     cudaFree(A); cudaFree(x); cudaFree(y); cudaFree(flush);
   }
