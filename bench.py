@@ -6,8 +6,12 @@
 A step is the reference's hot path on one batch of synthetic input
 (BASELINE.json configs[C], default C = 1: Nb = 20,000 wing nodes,
 Nv = 2,000,000 volume nodes, GCB m = 32, R = 2, tol = 1e-4 max|d|, FP64):
-the full selection loop including the final sweep (device resident, rank 0)
-followed by deform_points over all Nv volume nodes (sharded over ranks).
+the full selection loop including the final sweep (device resident)
+followed by deform_points over all Nv volume nodes. With N > 1 GPUs
+(torchrun): configs 0-1 run N independent replicas (weak scaling; they are
+too small to shard); configs 2-3 run the selection on rank 0,
+broadcast the support set (NCCL) and shard the volume (strong scaling).
+`--multi` overrides the choice.
 
 Metric: RBF pair-evaluations per second, whole job, with
 pairs = sum_i card(G_i) * Nc(i) + Nb * Nc   (selection, = cum_kernel_evals)
@@ -49,6 +53,10 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=100_000, help="volume targets in the CPU sample")
+    ap.add_argument("--multi", choices=["auto", "replicas", "shard"], default="auto",
+                    help="N > 1: independent replicas (weak scaling; auto for configs 0-1, too small "
+                         "to shard, SURVEY.md 8(e)) or selection on rank 0 + volume sharded (strong; "
+                         "auto for configs 2-3)")
     return ap.parse_args()
 
 
@@ -65,7 +73,15 @@ def workload(cfg):
     return W.config(cfg)
 
 
-def config_desc(wl, world, extra=None):
+def multi_mode(args, world):
+    if world == 1:
+        return "single"
+    if args.multi != "auto":
+        return args.multi
+    return "replicas" if args.config in (0, 1) else "shard"
+
+
+def config_desc(wl, world, extra=None, mode="single"):
     d = {
         "workload": f"BASELINE configs[{wl.name[-1]}]: {wl.name} wing, Nb={wl.nb}, Nv={wl.nv}, "
                     f"GCB m={wl.m}, R={wl.radius}, tol=1e-4*max|d|, seed={wl.seed}",
@@ -74,7 +90,9 @@ def config_desc(wl, world, extra=None):
         "m": wl.m,
         "radius": wl.radius,
         "tol": wl.tol,
-        "parallelism": f"selection on rank 0, volume sharded over {world} GPU(s)",
+        "parallelism": (f"{world} independent replicas (each GPU runs the whole step)"
+                        if mode == "replicas" else
+                        f"selection on rank 0, volume sharded over {world} GPU(s)"),
         "l2": "flushed between timed steps (256 MiB write)",
     }
     if extra:
@@ -268,22 +286,24 @@ def run_ours(args, rank, world, local):
 
     wl = workload(args.config)
     peak = measure_fp64_peak()
+    mode = multi_mode(args, world)
+    replicas = mode == "replicas"
     boundary = P.stage_boundary(P.BoundarySet(np.arange(wl.nb), wl.points, wl.disp))
     cfg = P.SelectionConfig(radius=wl.radius, tol=wl.tol, max_supports=wl.nb, m=wl.m, seed=wl.seed)
-    lo, hi = multi.shard_range(wl.nv, rank, world)
+    lo, hi = (0, wl.nv) if replicas else multi.shard_range(wl.nv, rank, world)
     nv_local = hi - lo
     vol_d = torch.from_numpy(np.ascontiguousarray(wl.volume[lo:hi])).cuda()
     out_d = torch.empty_like(vol_d)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def select_and_share():
-        if rank == 0:
+        if replicas or rank == 0:
             res = P.gcb_select(boundary, cfg)
             sp = torch.from_numpy(res.support.points).cuda()
             sw = torch.from_numpy(res.support.weights).cuda()
         else:
             res, sp, sw = None, None, torch.empty((0, 3), dtype=torch.float64, device="cuda")
-        if world > 1:
+        if world > 1 and not replicas:
             sp, sw = multi.broadcast_support(sp, sw)
         return res, sp, sw
 
@@ -323,10 +343,10 @@ def run_ours(args, rank, world, local):
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        if rank == 0:
+        if replicas or rank == 0:
             res2 = P.gcb_select(P.BoundarySet(np.arange(wl.nb), wl.points, wl.disp), cfg)
             sup = res2.support
-        if world > 1:
+        if world > 1 and not replicas:
             if rank == 0:
                 sp2, sw2 = torch.from_numpy(sup.points).cuda(), torch.from_numpy(sup.weights).cuda()
             else:
@@ -354,7 +374,7 @@ def run_ours(args, rank, world, local):
         a_sel = int(a.item())
     else:
         t_total, e2e_total = t_local, e2e_local
-    pairs_per_step = a_sel + wl.nv * nc
+    pairs_per_step = (a_sel + wl.nv * nc) * (world if replicas else 1)
     value = pairs_per_step * args.steps / t_total
     e2e_value = pairs_per_step * args.steps / e2e_total
 
@@ -406,9 +426,10 @@ def run_ours(args, rank, world, local):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_total / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak" if replicas else "strong",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, paper_2004_04817_b200/workloads.py)",
-            "config": config_desc(wl, world),
+            "config": config_desc(wl, world, mode=mode),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps * 1e3},
             "roofline": roof,
