@@ -90,9 +90,10 @@ def config_desc(wl, world, extra=None, mode="single"):
         "m": wl.m,
         "radius": wl.radius,
         "tol": wl.tol,
-        "parallelism": (f"{world} independent replicas (each GPU runs the whole step)"
+        "parallelism": ("1 GPU" if mode == "single" else
+                        f"{world} independent replicas (each GPU runs the whole step)"
                         if mode == "replicas" else
-                        f"selection on rank 0, volume sharded over {world} GPU(s)"),
+                        f"selection on rank 0, volume sharded over {world} GPUs"),
         "l2": "flushed between timed steps (256 MiB write)",
     }
     if extra:
