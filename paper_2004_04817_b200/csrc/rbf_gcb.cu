@@ -371,60 +371,93 @@ struct GlobalPath {
         t0 += kLoopThreads;
         continue;
       }
-      // tail round: rem rows, S = a power of two <= 32 lanes per row
-      int S = 32;
-      while (S > 1 && rem * S > kLoopThreads) S >>= 1;
-      while (S > 1 && (S >> 1) >= n) S >>= 1;
-      const int g = tid / S, sub = tid % S;
-      const bool active = g < rem;
-      const int t = t0 + g;
-      if (tid < rem) {  // prefetch row tid's epilogue operands
-        const int tt = t0 + tid;
-        const int pos = gpos ? __ldg(gpos + tt) : tt;
-        const bool elig = !__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + pos);
-        mpos[tid] = elig ? pos : ~pos;
-        md[3 * tid] = __ldcg(gdisp + 3 * (int64_t)tt);
-        md[3 * tid + 1] = __ldcg(gdisp + 3 * (int64_t)tt + 1);
-        md[3 * tid + 2] = __ldcg(gdisp + 3 * (int64_t)tt + 2);
-      }
-      double px = 0.0, py = 0.0, pz = 0.0;
-      if (active) {
-        px = __ldcg(gpt + 3 * (int64_t)t) * inv_r;
-        py = __ldcg(gpt + 3 * (int64_t)t + 1) * inv_r;
-        pz = __ldcg(gpt + 3 * (int64_t)t + 2) * inv_r;
-      }
-      double ax = 0.0, ay = 0.0, az = 0.0;
-      for (int s0 = 0; s0 < n; s0 += kSupTile) {
-        const int cnt = min(kSupTile, n - s0);
-        if (!staged || n > kSupTile) {
-          stage(s0, cnt);
-          staged = true;
-        }
-        if (active) {
-#pragma unroll 4
-          for (int j = sub; j < cnt; j += S)
-            pair_accum(px, py, pz, sh.sx[j], sh.sy[j], sh.sz[j], sh.wx[j], sh.wy[j], sh.wz[j], ax, ay, az);
-        }
-      }
-      if (t0 == lo) pc.mark(11);
-      for (int off = S >> 1; off > 0; off >>= 1) {
-        ax += __shfl_xor_sync(0xffffffffu, ax, off);
-        ay += __shfl_xor_sync(0xffffffffu, ay, off);
-        az += __shfl_xor_sync(0xffffffffu, az, off);
-      }
-      __syncthreads();  // prefetched operands visible
-      if (active && sub == 0) {
-        const int mp = mpos[g];
-        const bool elig = mp >= 0;
-        finish_row(t, elig ? mp : ~mp, elig, md[3 * g], md[3 * g + 1], md[3 * g + 2], ax, ay, az);
-      }
-      __syncthreads();
+      // tail round: rem rows over the warps, kT rows per lane group
+      if (rem > kLoopWarps)
+        tail_round<2>(gpos, gpt, gdisp, t0, rem, n, md, mpos, staged, lo, stage, finish_row);
+      else
+        tail_round<1>(gpos, gpt, gdisp, t0, rem, n, md, mpos, staged, lo, stage, finish_row);
       t0 += rem;
     }
     pc.mark(13);
     publish(cta_best(sh.cm, bu, 0), 0, par);
     publish(cta_best(sh.cm, br, 1), 1, par);
     pc.mark(14);
+  }
+
+  // The last round of a scan: rem (< 512) rows, kT rows per group of S lanes
+  // (S the largest power of two <= 32 with groups * S <= 512, and S <= n);
+  // each lane takes supports j = sub (mod S) for its kT rows (kT = 2 doubles
+  // the independent pair chains per lane once rem > 16), a butterfly combines
+  // the S partials, lane sub = 0 finishes the group's rows from the operands
+  // prefetched into shared memory.
+  template <int kT, class Stage, class FinishRow>
+  __device__ __forceinline__ void tail_round(const int* gpos, const double* gpt, const double* gdisp, int t0,
+                                             int rem, int n, double* md, int* mpos, bool& staged, int lo,
+                                             Stage& stage, FinishRow& finish_row) {
+    const int tid = threadIdx.x;
+    const int groups = (rem + kT - 1) / kT;
+    int S = 32;
+    while (S > 1 && groups * S > kLoopThreads) S >>= 1;
+    while (S > 1 && (S >> 1) >= n) S >>= 1;
+    const int g = tid / S, sub = tid % S;
+    const bool active = g < groups;
+    if (tid < rem) {  // prefetch row tid's epilogue operands
+      const int tt = t0 + tid;
+      const int pos = gpos ? __ldg(gpos + tt) : tt;
+      const bool elig = !__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + pos);
+      mpos[tid] = elig ? pos : ~pos;
+      md[3 * tid] = __ldcg(gdisp + 3 * (int64_t)tt);
+      md[3 * tid + 1] = __ldcg(gdisp + 3 * (int64_t)tt + 1);
+      md[3 * tid + 2] = __ldcg(gdisp + 3 * (int64_t)tt + 2);
+    }
+    double px[kT], py[kT], pz[kT], ax[kT], ay[kT], az[kT];
+#pragma unroll
+    for (int q = 0; q < kT; ++q) {
+      const int r = kT * g + q;
+      const bool ok = active && r < rem;
+      const int t = t0 + r;
+      px[q] = ok ? __ldcg(gpt + 3 * (int64_t)t) * inv_r : 0.0;
+      py[q] = ok ? __ldcg(gpt + 3 * (int64_t)t + 1) * inv_r : 0.0;
+      pz[q] = ok ? __ldcg(gpt + 3 * (int64_t)t + 2) * inv_r : 0.0;
+      ax[q] = ay[q] = az[q] = 0.0;
+    }
+    for (int s0 = 0; s0 < n; s0 += kSupTile) {
+      const int cnt = min(kSupTile, n - s0);
+      if (!staged || n > kSupTile) {
+        stage(s0, cnt);
+        staged = true;
+      }
+      if (active) {
+#pragma unroll 4
+        for (int j = sub; j < cnt; j += S) {
+          const double sx = sh.sx[j], sy = sh.sy[j], sz = sh.sz[j];
+          const double wx = sh.wx[j], wy = sh.wy[j], wz = sh.wz[j];
+#pragma unroll
+          for (int q = 0; q < kT; ++q) pair_accum(px[q], py[q], pz[q], sx, sy, sz, wx, wy, wz, ax[q], ay[q], az[q]);
+        }
+      }
+    }
+    if (t0 == lo) pc.mark(11);
+#pragma unroll
+    for (int q = 0; q < kT; ++q) {
+      for (int off = S >> 1; off > 0; off >>= 1) {
+        ax[q] += __shfl_xor_sync(0xffffffffu, ax[q], off);
+        ay[q] += __shfl_xor_sync(0xffffffffu, ay[q], off);
+        az[q] += __shfl_xor_sync(0xffffffffu, az[q], off);
+      }
+    }
+    __syncthreads();  // prefetched operands visible
+    if (active && sub == 0) {
+#pragma unroll
+      for (int q = 0; q < kT; ++q) {
+        const int r = kT * g + q;
+        if (r >= rem) continue;
+        const int mp = mpos[r];
+        const bool elig = mp >= 0;
+        finish_row(t0 + r, elig ? mp : ~mp, elig, md[3 * r], md[3 * r + 1], md[3 * r + 2], ax[q], ay[q], az[q]);
+      }
+    }
+    __syncthreads();
   }
 
   // Products with the n vectors of a packed triangle: rows of a row-packed

