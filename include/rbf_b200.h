@@ -251,6 +251,11 @@ RBF_API int rbf_partition(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
  * `scratch` holds rbf_fp64_probe_scratch_bytes(device) bytes; `flops_host`
  * receives the FP64 operations the launch performs (time it with events).
  */
+/* Return the persisting-L2 lines the L2-path selection launch keeps for Li
+ * (an access-policy window) to normal status; call once a selection has
+ * finished (bound by the Python layer after rbf_gcb_run). */
+RBF_API int rbf_l2_release(void);
+
 RBF_API size_t rbf_fp64_probe_scratch_bytes(int device);
 RBF_API int rbf_fp64_probe(int iters, double* scratch, double* flops_host, void* stream);
 

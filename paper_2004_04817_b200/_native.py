@@ -133,6 +133,7 @@ SIGNATURES = [
     ("rbf_partition", ctypes.c_int,
      [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64,
       ctypes.c_int64, c_dp, c_dp]),
+    ("rbf_l2_release", ctypes.c_int, []),
     ("rbf_fp64_probe_scratch_bytes", ctypes.c_size_t, [ctypes.c_int]),
     ("rbf_fp64_probe", ctypes.c_int, [ctypes.c_int, c_dp, ctypes.POINTER(ctypes.c_double), c_dp]),
 ]

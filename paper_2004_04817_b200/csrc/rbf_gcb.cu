@@ -2030,6 +2030,26 @@ extern "C" size_t rbf_gcb_scratch_bytes(int32_t nb, int32_t cap, int32_t ctas) {
   return total;
 }
 
+// Persisting-L2 set-aside for the L2 path (0: unavailable or disabled with
+// RBF_L2_PERSIST=0). The device limit is raised once, to the device maximum.
+static size_t l2_persist_bytes() {
+  static size_t bytes = [] {
+    const char* e = getenv("RBF_L2_PERSIST");
+    if (e && e[0] == '0') return (size_t)0;
+    int dev = 0, persist = 0, window = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return (size_t)0;
+    cudaDeviceGetAttribute(&persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    if (persist <= 0 || window <= 0) return (size_t)0;
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)persist) != cudaSuccess) {
+      cudaGetLastError();
+      return (size_t)0;
+    }
+    return (size_t)(persist < window ? persist : window);
+  }();
+  return bytes;
+}
+
 extern "C" int rbf_gcb_run(const rbf_gcb_args* args, void* stream) {
   if (!args) return set_error(RBF_EARG, "null args");
   const rbf_gcb_args& a = *args;
@@ -2063,9 +2083,38 @@ extern "C" int rbf_gcb_run(const rbf_gcb_args* args, void* stream) {
   } else {
     const size_t smem = sizeof(GlobalShared);
     RBF_CUDA_TRY(cudaFuncSetAttribute(gcb_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    void* kargs[] = {&acopy, &s};
-    RBF_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)gcb_grid_kernel, dim3(ctas), dim3(kLoopThreads),
-                                             kargs, smem, st));
+    // Li is read twice per append (c0 = Li row, c = c0 + Li r): keep its first
+    // persisting-L2 share resident (an access-policy window on this launch),
+    // while L and the column copy stream from HBM. rbf_l2_release() returns
+    // the lines to normal once the selection is over.
+    cudaLaunchAttribute attrs[2];
+    attrs[0].id = cudaLaunchAttributeCooperative;
+    attrs[0].val.cooperative = 1;
+    int nattr = 1;
+    const size_t persist = l2_persist_bytes();
+    if (persist > 0) {
+      const size_t li_bytes = sizeof(double) * (size_t)a.cap * (a.cap + 1) / 2;
+      attrs[1].id = cudaLaunchAttributeAccessPolicyWindow;
+      attrs[1].val.accessPolicyWindow.base_ptr = a.Li;
+      attrs[1].val.accessPolicyWindow.num_bytes = li_bytes < persist ? li_bytes : persist;
+      attrs[1].val.accessPolicyWindow.hitRatio = 1.0f;
+      attrs[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attrs[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      nattr = 2;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(kLoopThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attrs;
+    cfg.numAttrs = nattr;
+    RBF_CUDA_TRY(cudaLaunchKernelEx(&cfg, gcb_grid_kernel, acopy, s));
   }
+  return RBF_OK;
+}
+
+extern "C" int rbf_l2_release(void) {
+  if (l2_persist_bytes() > 0) RBF_CUDA_TRY(cudaCtxResetPersistingL2Cache());
   return RBF_OK;
 }

@@ -544,6 +544,7 @@ def _gcb_run(boundary, config, mode=None):
     args.dup_dist = NEAR_DUPLICATE_FRACTION * config.radius
     stream = N.stream_ptr()
     limit = min(config.max_supports, nb) + 1
+    used_grid = False
     while True:
         args.L, args.Li, args.y = buf.L.data_ptr(), buf.Li.data_ptr(), buf.y.data_ptr()
         args.sup, args.sel, args.inel = buf.sup.data_ptr(), buf.sel.data_ptr(), buf.inel.data_ptr()
@@ -551,6 +552,7 @@ def _gcb_run(boundary, config, mode=None):
         args.records, args.rec_cap = buf.records.data_ptr(), buf.rec_cap
         args.state = buf.state.data_ptr()
         args.scratch, args.scratch_bytes = buf.scratch.data_ptr(), buf.scratch_bytes
+        used_grid = used_grid or args.mode == N.GCB_GRID
         with N.launching("rbf_gcb_run", kernels=1):
             rc = lib.rbf_gcb_run(N.ctypes.byref(args), stream)
         N.check(rc, "rbf_gcb_run")
@@ -585,6 +587,8 @@ def _gcb_run(boundary, config, mode=None):
         if st.n_records >= buf.rec_cap:
             buf._grow_records(2 * buf.rec_cap, st.n_records)
 
+    if used_grid:
+        N.check(lib.rbf_l2_release(), "rbf_l2_release")
     n = st.n
     nrec = st.n_records
     sel, weights, recs = buf.unpack(host, n, nrec)
