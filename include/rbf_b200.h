@@ -46,6 +46,8 @@ enum {
   RBF_ENOTPD = 3,   /* NotPositiveDefiniteError (errors.py:13-15)            */
   RBF_EGROW = 5,    /* selection loop paused: factor/record capacity full    */
   RBF_ESTALL = 6,   /* SelectionStalledError (errors.py:44-46)               */
+  RBF_EPARSE = 7,   /* text not parsed natively: the caller re-parses it with
+                       the reference grammar for the exact ParseError      */
   RBF_ENCCL = 4     /* reserved: collective error                            */
 };
 
@@ -251,6 +253,33 @@ RBF_API int rbf_partition(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
  * `scratch` holds rbf_fp64_probe_scratch_bytes(device) bytes; `flops_host`
  * receives the FP64 operations the launch performs (time it with events).
  */
+/* ---------------------------------------------------------------------
+ * MDK1 / MDK1-DISP text codec (host, multi-threaded).  Replaces the bulk
+ * of meshio.py:135-250 (`read_mesh`, `write_mesh`, `read_displacements`,
+ * `write_displacements`). Readers accept exactly the inputs the reference
+ * parses the same way and return RBF_EPARSE for everything else (malformed
+ * text, and tokens outside the plain numeric grammar), on which the Python
+ * layer re-parses with the reference grammar to raise its ParseError /
+ * InvariantViolationError with the line number. `threads` <= 0: all cores.
+ *
+ * rbf_mdk1_counts: node / boundary / cell counts (counts[3]).
+ * rbf_mdk1_parse:  nodes (nv,3), boundary (nb, file order), cells (ne,5):
+ *                  arity then 3-4 node indices.
+ * rbf_disp_parse:  (nb,3) displacements aligned with the sorted boundary.
+ * rbf_mdk1_format_nodes / rbf_disp_format: canonical "%.17g" rows into
+ *                  `out` (100 / 124 bytes per row suffice); bytes written
+ *                  or -1.
+ */
+RBF_API int rbf_mdk1_counts(const char* text, size_t len, int64_t* counts, int threads);
+RBF_API int rbf_mdk1_parse(const char* text, size_t len, int64_t nv, int64_t nb, int64_t ne,
+                   double* nodes, int64_t* boundary, int64_t* cells, int threads);
+RBF_API int rbf_disp_parse(const char* text, size_t len, const int64_t* boundary, int64_t nb,
+                   double* disp, int threads);
+RBF_API int64_t rbf_mdk1_format_nodes(const double* xyz, int64_t n, char* out, int64_t cap,
+                              int threads);
+RBF_API int64_t rbf_disp_format(const int64_t* idx, const double* xyz, int64_t n, char* out,
+                        int64_t cap, int threads);
+
 /* Return the persisting-L2 lines the L2-path selection launch keeps for Li
  * (an access-policy window) to normal status; call once a selection has
  * finished (bound by the Python layer after rbf_gcb_run). */

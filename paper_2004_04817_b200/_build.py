@@ -13,7 +13,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "librbf_b200.so"
-SOURCES = ["rbf_capi.cu", "rbf_eval.cu", "rbf_chol.cu", "rbf_gcb.cu"]
+SOURCES = ["rbf_capi.cu", "rbf_eval.cu", "rbf_chol.cu", "rbf_gcb.cu", "rbf_meshio.cpp"]
 HEADERS = ["rbf_common.cuh", "rbf_tri.cuh", "rbf_internal.h"]
 
 NVCC_FLAGS = [
@@ -21,6 +21,9 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17", "--extended-lambda",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
 ]
+
+
+CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-fvisibility=hidden", "-pthread"]
 
 
 def _nvcc():
@@ -45,7 +48,12 @@ def build(force=False, verbose=False):
     objs = []
     for src in SOURCES:
         obj = LIBDIR / (Path(src).stem + ".o")
-        cmd = [_nvcc(), *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        if src.endswith(".cpp"):  # host code: the system C++ compiler
+            cuda_inc = str(Path(_nvcc()).resolve().parent.parent / "include")
+            cmd = [os.environ.get("CXX", "g++"), *CXX_FLAGS, "-I", cuda_inc, "-c", str(CSRC / src),
+                   "-o", str(obj)]
+        else:
+            cmd = [_nvcc(), *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)

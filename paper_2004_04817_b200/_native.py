@@ -21,6 +21,7 @@ RBF_ENOTPD = 3
 RBF_ENCCL = 4
 RBF_EGROW = 5
 RBF_ESTALL = 6
+RBF_EPARSE = 7
 STATUS_DONE = 1
 GCB_AUTO = 0
 GCB_CLUSTER = 1
@@ -134,6 +135,13 @@ SIGNATURES = [
      [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64,
       ctypes.c_int64, c_dp, c_dp]),
     ("rbf_l2_release", ctypes.c_int, []),
+    ("rbf_mdk1_counts", ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]),
+    ("rbf_mdk1_parse", ctypes.c_int,
+     [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, c_dp, c_dp, c_dp,
+      ctypes.c_int]),
+    ("rbf_disp_parse", ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, c_dp, ctypes.c_int64, c_dp, ctypes.c_int]),
+    ("rbf_mdk1_format_nodes", ctypes.c_int64, [c_dp, ctypes.c_int64, c_dp, ctypes.c_int64, ctypes.c_int]),
+    ("rbf_disp_format", ctypes.c_int64, [c_dp, c_dp, ctypes.c_int64, c_dp, ctypes.c_int64, ctypes.c_int]),
     ("rbf_fp64_probe_scratch_bytes", ctypes.c_size_t, [ctypes.c_int]),
     ("rbf_fp64_probe", ctypes.c_int, [ctypes.c_int, c_dp, ctypes.POINTER(ctypes.c_double), c_dp]),
 ]

@@ -96,7 +96,7 @@ def volume_sample(wl, support, radius, n=4096):
 
 
 def main():
-    if len(sys.argv) > 1 and sys.argv[1] == "metrics":  # only the metrics case
+    if len(sys.argv) > 1 and sys.argv[1] in ("metrics", "meshio"):  # only these cases
         return metrics_only()
     # 1. explicit small inputs (stored)
     pts, disp = hemisphere()
@@ -152,6 +152,26 @@ def main():
          hist_rms=np.array([h.rms_error for _, h in hist]),
          hist_node=np.array([h.node_of_max for _, h in hist]), radius=np.array(3.0))
 
+    # 2c. meshio (reference meshio.py): canonical writer output, for byte parity
+    from rbfdeform import meshio as RIO
+
+    rng = np.random.default_rng(99)
+    nodes = rng.normal(size=(40, 3)) * np.array([1.0, 1e-7, 3e5])
+    nodes[0] = [0.0, -0.0, 1e-310]
+    nodes[1] = [1.0, 0.1, 123456789.0]
+    mesh = RIO.Mesh(nodes=nodes, boundary=np.array([5, 1, 30, 2]),
+                    cells=[np.array([0, 1, 2]), np.array([3, 4, 5, 6])])
+    disp = rng.normal(size=(4, 3)) * 1e-3
+    res = R.gcb_select(R.BoundarySet(np.arange(40), nodes[:, :3] * np.array([1.0, 1e7, 3e-6]),
+                                     rng.normal(size=(40, 3)) * 0.01),
+                       R.SelectionConfig(radius=3.0, tol=1e-6, max_supports=12, m=3, seed=1))
+    (HERE / "meshio_mesh.mdk1").write_text(RIO.write_mesh(mesh))
+    (HERE / "meshio_disp.mdk1").write_text(RIO.write_displacements(disp, mesh.boundary))
+    (HERE / "meshio_history.csv").write_text(RIO.write_history_csv(res.history))
+    (HERE / "meshio_supports.csv").write_text(RIO.write_supports_csv(res.support))
+    save("meshio_values", nodes=nodes, boundary=mesh.boundary, disp=disp,
+         sup_nodes=res.support.nodes, sup_points=res.support.points, sup_weights=res.support.weights)
+
     # 3. BASELINE configs (generator parameters + digest; outputs)
     for idx, ms in ((0, (1, 8)),):
         wl = W.config(idx, nv=100_000)
@@ -181,7 +201,7 @@ def main():
 
 def metrics_only():
     src = open(__file__).read()
-    a = src.index("    # 2b. metrics")
+    a = src.index("    # 2b. metrics") if "metrics" in sys.argv[1:] else src.index("    # 2c. meshio")
     b = src.index("    # 3. BASELINE configs")
     exec(compile("if True:\n" + src[a:b], __file__, "exec"), globals())
 
