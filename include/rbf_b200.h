@@ -71,6 +71,20 @@ RBF_API int rbf_eval(const double* targets, int64_t n_targets,
              const double* sup_points, const double* sup_weights, int64_t n_sup,
              double radius, int deform, double* out, void* stream);
 
+/* Host-resident variant of rbf_eval for inputs that live in host memory
+ * (the public numpy API: core.py:337-367): `host_targets` (n,3) are streamed
+ * through the caller's device buffers `dev_in` / `dev_out` (n,3 each) in
+ * `chunks` pieces (<= 63) on library-owned copy streams, so the
+ * host->device copy, the kernel and the device->host copy of consecutive
+ * pieces overlap (PCIe is full duplex). Results land in `host_out` (pinned
+ * memory for asynchronous copies) once `stream` is synchronised; bitwise
+ * equal to rbf_eval on the whole array. Support arrays are device pointers.
+ */
+RBF_API int rbf_eval_host(const double* host_targets, int64_t n_targets,
+                  const double* sup_points, const double* sup_weights, int64_t n_sup,
+                  double radius, int deform, double* dev_in, double* dev_out,
+                  double* host_out, int chunks, void* stream);
+
 /* ---------------------------------------------------------------------
  * Interpolation error at boundary rows, fused with the (err, lowest id)
  * arg-max.  Replaces selection.py:215-221 `_errors_at` +

@@ -116,6 +116,9 @@ SIGNATURES = [
      [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     ("rbf_eval", ctypes.c_int,
      [c_dp, ctypes.c_int64, c_dp, c_dp, ctypes.c_int64, ctypes.c_double, ctypes.c_int, c_dp, c_dp]),
+    ("rbf_eval_host", ctypes.c_int,
+     [c_dp, ctypes.c_int64, c_dp, c_dp, ctypes.c_int64, ctypes.c_double, ctypes.c_int, c_dp, c_dp, c_dp,
+      ctypes.c_int, c_dp]),
     ("rbf_errors_scratch_bytes", ctypes.c_size_t, [ctypes.c_int64]),
     ("rbf_errors_argmax", ctypes.c_int,
      [c_dp, c_dp, c_dp, ctypes.c_int64, c_dp, c_dp, ctypes.c_int64, ctypes.c_double, c_dp,

@@ -296,48 +296,26 @@ def eval_device(points, support_points, weights, radius, deform=False, out=None)
 
 _PIPELINE_MIN = 1 << 18   # host inputs at least this long are streamed in chunks
 _PIPELINE_CHUNKS = 8
-_streams = {}
-
-
-def _pipeline_streams():
-    t = N.torch()
-    dev = t.cuda.current_device()
-    if dev not in _streams:
-        _streams[dev] = (t.cuda.Stream(), t.cuda.Stream())
-    return _streams[dev]
 
 
 def _eval_host_pipelined(points, s, w, radius, deform):
-    """Host (n, 3) points -> host result, the n targets streamed in chunks so
-    the host->device copy of chunk k+1 and the device->host copy of chunk
-    k-1 overlap the kernel on chunk k (PCIe is full duplex). Per-target
-    results are bitwise those of one launch."""
+    """Host (n, 3) points -> host result through the library's chunked
+    copy / kernel / copy pipeline (rbf_eval_host): the host->device copy of
+    chunk k+1 and the device->host copy of chunk k-1 overlap the kernel on
+    chunk k. Per-target results are bitwise those of one launch."""
+    lib = N.require_cuda()
     t = N.torch()
     n = len(points)
-    src = t.from_numpy(points)  # pinned memory streams asynchronously; pageable copies block per chunk
+    src = t.from_numpy(points)  # pinned memory copies asynchronously; pageable ones are staged
     dev_in = t.empty((n, 3), dtype=t.float64, device=_device())
     dev_out = t.empty((n, 3), dtype=t.float64, device=_device())
     host_out = t.empty((n, 3), dtype=t.float64, pin_memory=True)
-    copy_in, copy_out = _pipeline_streams()
-    compute = t.cuda.current_stream()
-    step = -(-n // _PIPELINE_CHUNKS)
-    step = -(-step // 512) * 512
-    for lo in range(0, n, step):
-        hi = min(n, lo + step)
-        with t.cuda.stream(copy_in):
-            dev_in[lo:hi].copy_(src[lo:hi], non_blocking=True)
-            ready = t.cuda.Event()
-            ready.record(copy_in)
-        compute.wait_event(ready)
-        eval_device(dev_in[lo:hi], s, w, radius, deform=deform, out=dev_out[lo:hi])
-        done = t.cuda.Event()
-        done.record(compute)
-        copy_out.wait_event(done)
-        with t.cuda.stream(copy_out):
-            host_out[lo:hi].copy_(dev_out[lo:hi], non_blocking=True)
-    copy_out.synchronize()
-    # keep the device buffers alive until the copies that use them are done
-    compute.wait_stream(copy_out)
+    with N.launching("rbf_eval", kernels=_PIPELINE_CHUNKS):
+        rc = lib.rbf_eval_host(src.data_ptr(), n, N.dptr(s), N.dptr(w), s.shape[0], float(radius),
+                               1 if deform else 0, N.dptr(dev_in), N.dptr(dev_out), host_out.data_ptr(),
+                               _PIPELINE_CHUNKS, N.stream_ptr())
+    N.check(rc, "rbf_eval_host")
+    t.cuda.current_stream().synchronize()
     return host_out.numpy()
 
 

@@ -49,3 +49,20 @@ for chunks in (4, 8, 16, 32):
 h = torch.empty((wl.nv, 3), dtype=torch.float64, pin_memory=True)
 print("H2D 48 MB pinned        %.3f ms" % timed(lambda: vol_d.copy_(torch.from_numpy(vol), non_blocking=True)))
 print("D2H 48 MB pinned        %.3f ms" % timed(lambda: h.copy_(vol_d, non_blocking=True)))
+
+# duplex: H2D and D2H of 48 MB each on two streams at once
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+vol_d2 = torch.empty_like(vol_d)
+src = torch.from_numpy(vol)
+
+
+def duplex():
+    with torch.cuda.stream(s1):
+        vol_d2.copy_(src, non_blocking=True)
+    with torch.cuda.stream(s2):
+        h.copy_(vol_d, non_blocking=True)
+    s1.synchronize()
+    s2.synchronize()
+
+
+print("H2D || D2H 48 MB each   %.3f ms" % timed(duplex))
