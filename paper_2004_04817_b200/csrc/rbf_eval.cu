@@ -20,8 +20,6 @@ namespace rbf {
 constexpr int kEvalThreads = 128;
 constexpr int kEvalTPT = 4;
 constexpr int kEvalTile = 128;
-constexpr int kEvalTargetsPerBlock = kEvalThreads * kEvalTPT;
-
 enum EvalMode { kModeEval = 0, kModeDeform = 1, kModeError = 2 };
 
 template <int MODE, int kEvalThreads = rbf::kEvalThreads, int kEvalTPT = rbf::kEvalTPT,
@@ -192,10 +190,6 @@ __global__ void best_reduce_kernel(const Best* __restrict__ partials, int n, dou
   }
 }
 
-static inline int64_t eval_blocks(int64_t nt) {
-  return (nt + kEvalTargetsPerBlock - 1) / kEvalTargetsPerBlock;
-}
-
 // Launch variants of the volume kernel: 0 the expanded pair form (128
 // threads x 6 targets), 1-5 the difference form at several geometries
 // (threads, targets per thread, support tile, min resident blocks), 6 the
@@ -328,8 +322,15 @@ extern "C" int rbf_eval_host(const double* host_targets, int64_t n_targets, cons
   return RBF_OK;
 }
 
+// Error scans use the volume kernel's launch shape (128 threads x 6 rows, 3
+// CTAs per SM); 2 / 4 rows per thread and 64-thread blocks measured within
+// 5 % of it on configs[3]'s boundary (tools/err_kernel_time.py).
+constexpr int kErrThreads = 128, kErrTPT = 6, kErrMinBlocks = 3;
+constexpr int kErrRowsPerBlock = kErrThreads * kErrTPT;
+
 extern "C" size_t rbf_errors_scratch_bytes(int64_t n_targets) {
-  return 256 + (size_t)eval_blocks(n_targets < 1 ? 1 : n_targets) * sizeof(Best);
+  const int64_t nt = n_targets < 1 ? 1 : n_targets;
+  return 256 + (size_t)((nt + kErrRowsPerBlock - 1) / kErrRowsPerBlock) * sizeof(Best);
 }
 
 extern "C" int rbf_errors_argmax(const double* bnd_points, const double* bnd_disp,
@@ -343,13 +344,15 @@ extern "C" int rbf_errors_argmax(const double* bnd_points, const double* bnd_dis
   if (!bnd_points || !bnd_disp || !scratch) return set_error(RBF_EARG, "null pointer");
   if (scratch_bytes < rbf_errors_scratch_bytes(n_targets))
     return set_error(RBF_EARG, "scratch too small");
-  const int64_t nblk = eval_blocks(n_targets);
+  int64_t nblk = 0;
   cudaStream_t s = as_stream(stream);
   double* result = reinterpret_cast<double*>(scratch);
   Best* partials = reinterpret_cast<Best*>(static_cast<char*>(scratch) + 256);
-  eval_kernel<kModeError><<<(unsigned)nblk, kEvalThreads, 0, s>>>(
-      bnd_points, bnd_disp, positions, n_targets, sup_points, sup_weights, (int)n_sup,
-      1.0 / radius, err_out, partials);
+  const double inv_r = 1.0 / radius;
+  nblk = (n_targets + kErrRowsPerBlock - 1) / kErrRowsPerBlock;
+  eval_kernel<kModeError, kErrThreads, kErrTPT, 128, kErrMinBlocks><<<(unsigned)nblk, kErrThreads, 0, s>>>(
+      bnd_points, bnd_disp, positions, n_targets, sup_points, sup_weights, (int)n_sup, inv_r, err_out,
+      partials);
   RBF_LAUNCH_CHECK("eval_kernel<error>");
   best_reduce_kernel<<<1, 256, 0, s>>>(partials, (int)nblk, result);
   RBF_LAUNCH_CHECK("best_reduce_kernel");
