@@ -441,6 +441,10 @@ def run_ours(args, rank, world, local):
             "gpu_launches": launches,
             "breakdown": {"nc": nc, "selection_pairs": a_sel, "volume_pairs": wl.nv * nc,
                           "iterations": len(res.history.records),
+                          # the reference's per-stage columns (cli.py:38), device clock:
+                          # t1 = error scans, t2 = solves/appends (selection.py:310-371)
+                          "t1_ms": 1e3 * sum(r.t1_s for r in res.history.records),
+                          "t2_ms": 1e3 * sum(r.t2_s for r in res.history.records),
                           "selection_ms": statistics.mean(sel_ms) if sel_ms else None,
                           "volume_ms": statistics.mean(vol_ms) if vol_ms else None,
                           "converged": bool(res.converged),
