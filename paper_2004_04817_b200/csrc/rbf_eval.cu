@@ -328,9 +328,112 @@ extern "C" int rbf_eval_host(const double* host_targets, int64_t n_targets, cons
 constexpr int kErrThreads = 128, kErrTPT = 6, kErrMinBlocks = 3;
 constexpr int kErrRowsPerBlock = kErrThreads * kErrTPT;
 
+// Small scans (a GCB group: a few hundred rows) would occupy a handful of
+// SMs with one row per thread; they are split over S slices of the supports
+// instead (grid = row blocks x S, partial sums through scratch, then one
+// fixed-order pass sums the slices per row and finishes residual + arg-max):
+// deterministic for a given (rows, supports).
+constexpr int kSplitThreads = 128, kSplitTPT = 2;
+constexpr int kSplitRowsPerBlock = kSplitThreads * kSplitTPT;
+constexpr int64_t kSplitBound = 148LL * 4 * kSplitRowsPerBlock;  // rows x slices held in scratch
+constexpr int kFinishThreads = 128;
+
+static int split_slices(int64_t nt, int64_t ns) {
+  if (nt >= kSplitBound / 2 || ns < 128) return 1;
+  const int64_t blocks = (nt + kSplitRowsPerBlock - 1) / kSplitRowsPerBlock;
+  int64_t S = (2 * 148 * 4 + blocks - 1) / blocks;  // ~2 waves of 4 CTAs per SM
+  S = std::min<int64_t>(S, ns / 64);                 // >= 64 supports per slice
+  S = std::min<int64_t>(S, kSplitBound / nt);
+  return (int)std::max<int64_t>(S, 1);
+}
+
+__global__ void __launch_bounds__(kSplitThreads, 4)
+err_partial_kernel(const double* __restrict__ tpts, const int64_t* __restrict__ pos, int64_t nt,
+                   const double* __restrict__ spts, const double* __restrict__ sw, int nsup, int per_slice,
+                   double inv_r, double* __restrict__ part) {
+  __shared__ double4 s_a[128];
+  __shared__ double2 s_b[128];
+  const int slice = blockIdx.y;
+  const int j0 = slice * per_slice, j1 = min(nsup, j0 + per_slice);
+  const int64_t base = (int64_t)blockIdx.x * kSplitRowsPerBlock + threadIdx.x;
+  double px[kSplitTPT], py[kSplitTPT], pz[kSplitTPT], ax[kSplitTPT], ay[kSplitTPT], az[kSplitTPT];
+#pragma unroll
+  for (int k = 0; k < kSplitTPT; ++k) {
+    const int64_t idx = base + (int64_t)k * kSplitThreads;
+    const int64_t r = idx < nt ? (pos ? pos[idx] : idx) : -1;
+    px[k] = r >= 0 ? tpts[3 * r] * inv_r : 0.0;
+    py[k] = r >= 0 ? tpts[3 * r + 1] * inv_r : 0.0;
+    pz[k] = r >= 0 ? tpts[3 * r + 2] * inv_r : 0.0;
+    ax[k] = ay[k] = az[k] = 0.0;
+  }
+  for (int t0 = j0; t0 < j1; t0 += 128) {
+    const int cnt = min(128, j1 - t0);
+    __syncthreads();
+    for (int j = threadIdx.x; j < cnt; j += kSplitThreads) {
+      const int g = t0 + j;
+      s_a[j] = make_double4(spts[3 * g] * inv_r, spts[3 * g + 1] * inv_r, spts[3 * g + 2] * inv_r, sw[3 * g]);
+      s_b[j] = make_double2(sw[3 * g + 1], sw[3 * g + 2]);
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int j = 0; j < cnt; ++j) {
+      const double4 a = s_a[j];
+      const double2 b = s_b[j];
+#pragma unroll
+      for (int k = 0; k < kSplitTPT; ++k)
+        pair_accum(px[k], py[k], pz[k], a.x, a.y, a.z, a.w, b.x, b.y, ax[k], ay[k], az[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kSplitTPT; ++k) {
+    const int64_t idx = base + (int64_t)k * kSplitThreads;
+    if (idx >= nt) continue;
+    double* o = part + 3 * ((int64_t)slice * nt + idx);
+    o[0] = ax[k];
+    o[1] = ay[k];
+    o[2] = az[k];
+  }
+}
+
+__global__ void __launch_bounds__(kFinishThreads)
+err_finish_kernel(const double* __restrict__ tdisp, const int64_t* __restrict__ pos, int64_t nt,
+                  const double* __restrict__ part, int S, double* __restrict__ err_out,
+                  Best* __restrict__ partials) {
+  const int64_t idx = (int64_t)blockIdx.x * kFinishThreads + threadIdx.x;
+  Best best{-1.0, 0x7fffffff};
+  if (idx < nt) {
+    double ux = 0.0, uy = 0.0, uz = 0.0;
+    for (int sl = 0; sl < S; ++sl) {  // slices in order: deterministic
+      const double* p = part + 3 * ((int64_t)sl * nt + idx);
+      ux += p[0];
+      uy += p[1];
+      uz += p[2];
+    }
+    const int64_t r = pos ? pos[idx] : idx;
+    const double e = residual_norm(tdisp[3 * r], tdisp[3 * r + 1], tdisp[3 * r + 2], ux, uy, uz);
+    if (err_out) err_out[idx] = e;
+    best = Best{e, (int)r};
+  }
+  best = warp_best(best);
+  __shared__ Best s_best[kFinishThreads / kWarp];
+  if ((threadIdx.x & 31) == 0) s_best[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Best b = s_best[0];
+    for (int w = 1; w < kFinishThreads / kWarp; ++w) b = best_of(b, s_best[w]);
+    partials[blockIdx.x] = b;
+  }
+}
+
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
 extern "C" size_t rbf_errors_scratch_bytes(int64_t n_targets) {
   const int64_t nt = n_targets < 1 ? 1 : n_targets;
-  return 256 + (size_t)((nt + kErrRowsPerBlock - 1) / kErrRowsPerBlock) * sizeof(Best);
+  const int64_t blocks = std::max((nt + kErrRowsPerBlock - 1) / kErrRowsPerBlock,
+                                  (nt + kFinishThreads - 1) / kFinishThreads);
+  size_t bytes = 256 + align256((size_t)blocks * sizeof(Best));
+  if (nt < kSplitBound / 2) bytes += (size_t)kSplitBound * 3 * sizeof(double);
+  return bytes;
 }
 
 extern "C" int rbf_errors_argmax(const double* bnd_points, const double* bnd_disp,
@@ -349,11 +452,28 @@ extern "C" int rbf_errors_argmax(const double* bnd_points, const double* bnd_dis
   double* result = reinterpret_cast<double*>(scratch);
   Best* partials = reinterpret_cast<Best*>(static_cast<char*>(scratch) + 256);
   const double inv_r = 1.0 / radius;
-  nblk = (n_targets + kErrRowsPerBlock - 1) / kErrRowsPerBlock;
-  eval_kernel<kModeError, kErrThreads, kErrTPT, 128, kErrMinBlocks><<<(unsigned)nblk, kErrThreads, 0, s>>>(
-      bnd_points, bnd_disp, positions, n_targets, sup_points, sup_weights, (int)n_sup, inv_r, err_out,
-      partials);
-  RBF_LAUNCH_CHECK("eval_kernel<error>");
+  const int S = split_slices(n_targets, n_sup);
+  if (S > 1) {
+    const int64_t blocks = (n_targets + kErrRowsPerBlock - 1) / kErrRowsPerBlock;
+    const int64_t fin = (n_targets + kFinishThreads - 1) / kFinishThreads;
+    double* part = reinterpret_cast<double*>(static_cast<char*>(scratch) + 256 +
+                                             align256((size_t)std::max(blocks, fin) * sizeof(Best)));
+    const int per_slice = (int)((n_sup + S - 1) / S);
+    const dim3 grid((unsigned)((n_targets + kSplitRowsPerBlock - 1) / kSplitRowsPerBlock), (unsigned)S);
+    err_partial_kernel<<<grid, kSplitThreads, 0, s>>>(bnd_points, positions, n_targets, sup_points, sup_weights,
+                                                       (int)n_sup, per_slice, inv_r, part);
+    RBF_LAUNCH_CHECK("err_partial_kernel");
+    nblk = fin;
+    err_finish_kernel<<<(unsigned)nblk, kFinishThreads, 0, s>>>(bnd_disp, positions, n_targets, part, S, err_out,
+                                                                 partials);
+    RBF_LAUNCH_CHECK("err_finish_kernel");
+  } else {
+    nblk = (n_targets + kErrRowsPerBlock - 1) / kErrRowsPerBlock;
+    eval_kernel<kModeError, kErrThreads, kErrTPT, 128, kErrMinBlocks><<<(unsigned)nblk, kErrThreads, 0, s>>>(
+        bnd_points, bnd_disp, positions, n_targets, sup_points, sup_weights, (int)n_sup, inv_r, err_out,
+        partials);
+    RBF_LAUNCH_CHECK("eval_kernel<error>");
+  }
   best_reduce_kernel<<<1, 256, 0, s>>>(partials, (int)nblk, result);
   RBF_LAUNCH_CHECK("best_reduce_kernel");
   if (best_host) {
