@@ -1,10 +1,11 @@
 """Support-node selection (greedy and grouped-circular greedy) on the B200.
 
-Drop-in mirror of reference ``selection.py``. The data types, the seeded
-PCG64 partition (selection.py:177-185) and the seeds (selection.py:198-212)
-stay numpy so they are bit-identical to the reference; the whole selection
-loop (``_gcb_run``, selection.py:274-421) runs as ONE cooperative
-persistent kernel of the sm_100a library (``rbf_gcb_run``,
+Drop-in mirror of reference ``selection.py``. The data types stay numpy;
+the seeded PCG64 partition (selection.py:177-185) is computed on the host
+by the library's restatement of numpy's PCG64 permutation (bit-identical,
+``rbf_partition``) and cached per (Nb, m, seed); the whole selection loop
+(``_gcb_run``, selection.py:274-421, seeds selection.py:198-212 included)
+runs as ONE persistent kernel of the sm_100a library (``rbf_gcb_run``,
 csrc/rbf_gcb.cu). The host reads the support set, weights and
 per-iteration records back once, at the end.
 
@@ -354,7 +355,7 @@ def _errors_device(positions, boundary, support_points, weights, radius, want_er
     nbytes = lib.rbf_errors_scratch_bytes(n)
     scratch = t.empty(nbytes, dtype=t.uint8, device=_device())
     best = (N.ctypes.c_double * 2)()
-    with N.launching("rbf_errors_argmax", kernels=2):
+    with N.launching("rbf_errors_argmax", kernels=3):
         rc = lib.rbf_errors_argmax(N.dptr(pts), N.dptr(disp), N.dptr(pos), n, N.dptr(sp), N.dptr(w),
                                    sp.shape[0], float(radius), N.dptr(err) if err is not None else None,
                                    best, N.dptr(scratch), nbytes, N.stream_ptr())
