@@ -648,3 +648,28 @@ def random_select(boundary, n, seed, radius):
 def error_stage_cost(history):
     """Error-stage kernel evaluations, final sweep excluded (selection.py:445-448)."""
     return sum(r.kernel_evals for r in history.records)
+
+
+def resolve_auto_m(boundary, radius, tol, seed=0, workers=1, probe_cap=200):
+    """Group count from a short greedy probe (reference cli.py:69-99,
+    ``--m auto``): greedy selection to the earlier of ``probe_cap`` supports
+    or the tolerance; if it did not converge, the final support count is
+    extrapolated from the log-error decay over the second half of the probe;
+    returns round(1.5 * Nb / Nc_hat) clipped to [1, Nb] (the middle of the
+    recommended [Nb/Nc, 2 Nb/Nc] band). The probe runs on the device."""
+    nb = len(boundary)
+    cap = min(probe_cap, nb)
+    probe = greedy_select(boundary, SelectionConfig(radius=radius, tol=tol, max_supports=max(cap, 3),
+                                                    seed=seed, workers=workers))
+    n_probe = len(probe.support)
+    if probe.converged:
+        n_hat = n_probe
+    else:
+        # m = 1 adds a node at every over-tolerance visit: record r holds 3 + r supports
+        err = np.array([r.local_max_error for r in probe.history.records])
+        count = 3.0 + np.arange(len(err))
+        half = slice(len(err) // 2, None)
+        slope, icpt = np.polyfit(count[half], np.log(np.maximum(err[half], 1e-300)), 1)
+        n_hat = nb if slope >= 0 else (np.log(tol) - icpt) / slope
+        n_hat = min(max(n_hat, n_probe), nb)
+    return int(np.clip(round(1.5 * nb / n_hat), 1, nb))

@@ -96,7 +96,7 @@ def volume_sample(wl, support, radius, n=4096):
 
 
 def main():
-    if len(sys.argv) > 1 and sys.argv[1] in ("metrics", "meshio"):  # only these cases
+    if len(sys.argv) > 1 and sys.argv[1] in ("metrics", "meshio", "auto_m"):  # from this case on
         return metrics_only()
     # 1. explicit small inputs (stored)
     pts, disp = hemisphere()
@@ -172,6 +172,16 @@ def main():
     save("meshio_values", nodes=nodes, boundary=mesh.boundary, disp=disp,
          sup_nodes=res.support.nodes, sup_points=res.support.points, sup_weights=res.support.weights)
 
+    # 2d. resolve_auto_m (reference cli.py:69-99) on configs[0]'s wing
+    from rbfdeform.cli import resolve_auto_m
+
+    wl0 = W.config(0, nv=10)
+    b0 = R.BoundarySet(indices=np.arange(wl0.nb), points=wl0.points, disp=wl0.disp)
+    cases = [(200, wl0.tol), (40, wl0.tol), (200, 1e-2)]
+    save("auto_m", caps=np.array([c for c, _ in cases]), tols=np.array([t for _, t in cases]),
+         m=np.array([resolve_auto_m(b0, wl0.radius, t, seed=0, probe_cap=c) for c, t in cases]),
+         digest=np.array(digest(wl0.points, wl0.disp)))
+
     # 3. BASELINE configs (generator parameters + digest; outputs)
     for idx, ms in ((0, (1, 8)),):
         wl = W.config(idx, nv=100_000)
@@ -201,7 +211,8 @@ def main():
 
 def metrics_only():
     src = open(__file__).read()
-    a = src.index("    # 2b. metrics") if "metrics" in sys.argv[1:] else src.index("    # 2c. meshio")
+    start = {"metrics": "    # 2b. metrics", "meshio": "    # 2c. meshio", "auto_m": "    # 2d. resolve_auto_m"}
+    a = src.index(start[sys.argv[1]])
     b = src.index("    # 3. BASELINE configs")
     exec(compile("if True:\n" + src[a:b], __file__, "exec"), globals())
 

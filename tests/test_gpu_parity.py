@@ -441,3 +441,13 @@ def test_selection_multi_cluster_msg_path(cuda, monkeypatch):
     res = _gcb_run(b, cfg, mode=N.GCB_MSG)
     assert np.array_equal(res.support.nodes, g["seq"])
     assert rel(res.support.weights, g["weights"]) <= 1e-9
+
+
+def test_resolve_auto_m_matches_reference_golden(cuda):
+    """--m auto's greedy probe + error-decay extrapolation (reference
+    cli.py:69-99) picks the reference's m."""
+    g = load_golden("auto_m")
+    wl = W.config(0, nv=10)
+    b = cuda.BoundarySet(np.arange(wl.nb), wl.points, wl.disp)
+    for cap, tol, m in zip(g["caps"], g["tols"], g["m"]):
+        assert cuda.resolve_auto_m(b, wl.radius, float(tol), seed=0, probe_cap=int(cap)) == int(m)
