@@ -451,3 +451,47 @@ def test_resolve_auto_m_matches_reference_golden(cuda):
     b = cuda.BoundarySet(np.arange(wl.nb), wl.points, wl.disp)
     for cap, tol, m in zip(g["caps"], g["tols"], g["m"]):
         assert cuda.resolve_auto_m(b, wl.radius, float(tol), seed=0, probe_cap=int(cap)) == int(m)
+
+
+def test_concurrent_selections_and_evaluations(cuda):
+    """Host threads may call the pure API concurrently (reference SPEC.md:131):
+    pooled loop buffers and the library's per-thread copy streams keep the
+    calls independent; results equal the serial ones."""
+    import threading
+
+    cases = ["smooth0_m5", "smooth3_m5", "hemisphere_m4", "cfg0_m8"]
+    serial = {}
+    inputs = {}
+    for name in cases:
+        g = load_golden(name)
+        pts, disp, _ = golden_inputs(name, g)
+        radius, tol, cap, m, seed = g["params"]
+        b = cuda.BoundarySet(np.arange(len(pts)), pts, disp)
+        cfg = cuda.SelectionConfig(radius=radius, tol=tol, max_supports=int(cap), m=int(m), seed=int(seed))
+        inputs[name] = (b, cfg)
+        serial[name] = cuda.gcb_select(b, cfg)
+    vol = np.random.default_rng(3).normal(size=(300_000, 3))
+    ref_u = cuda.evaluate_displacements(vol, serial["cfg0_m8"].support, 2.0)
+    out, errs = {}, []
+
+    def work(name):
+        try:
+            import torch
+
+            torch.cuda.set_device(0)
+            for _ in range(3):
+                out[name] = cuda.gcb_select(*inputs[name])
+            out[name + "_u"] = cuda.evaluate_displacements(vol, serial["cfg0_m8"].support, 2.0)
+        except Exception as exc:  # surfaced below
+            errs.append(exc)
+
+    threads = [threading.Thread(target=work, args=(n,)) for n in cases]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errs, errs
+    for name in cases:
+        assert np.array_equal(out[name].support.nodes, serial[name].support.nodes)
+        assert np.array_equal(out[name].support.weights, serial[name].support.weights)
+        assert np.array_equal(out[name + "_u"], ref_u)
