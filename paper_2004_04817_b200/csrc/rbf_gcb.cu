@@ -49,6 +49,10 @@ constexpr int kRowSmemMax = 8192;    // GlobalPath: row held in shared memory
 constexpr int kSmallMax = 1024;      // SmemPath: supports resident in shared memory
 constexpr int kAutoClusterMaxCard = 2048;
 constexpr int64_t kClusterScanPairs = 400000;  // per group scan, see gcb_driver
+// when the MSG path's resident capacity is reached, scans of more pairs than
+// this go to the grid rather than to the shared-memory cluster path
+// (configs[4] m = 187: 31.0 -> 23.6 ms; tools/greedy_ab.py)
+constexpr int64_t kSmemScanPairs = 150000;
 constexpr int kMsgDefaultClusters = 1;         // MSG path: clusters sharing the scans
 constexpr int kNone = 0x7fffffff;
 
@@ -1824,7 +1828,8 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
       return;
     }
     if (n >= Path::kMaxN - 1) {  // beyond this path's resident capacity
-      save(RBF_EGROW, self_mode == RBF_GCB_MSG ? RBF_GCB_SMEM
+      const bool big_scans = (int64_t)((a.nb + m - 1) / m) * n > kSmemScanPairs;
+      save(RBF_EGROW, self_mode == RBF_GCB_MSG ? (big_scans ? RBF_GCB_GRID : RBF_GCB_SMEM)
                       : self_mode == RBF_GCB_SMEM ? RBF_GCB_CLUSTER : self_mode);
       return;
     }
