@@ -253,6 +253,7 @@ struct GlobalShared {
   double sx[kSupTile], sy[kSupTile], sz[kSupTile];
   double wx[kSupTile], wy[kSupTile], wz[kSupTile];
   double row[kRowSmemMax];
+  double gred[kLoopWarps];  // row products: per-warp partials of a shared row
 };
 
 template <class Team>
@@ -472,8 +473,46 @@ struct GlobalPath {
   template <bool kCols, class XL, class Fin>
   __device__ __forceinline__ void tri_gemv(const double* A, int n, XL xload, Fin finish) {
     const int lane = threadIdx.x & 31;
-    const int gw = blockIdx.x * kLoopWarps + (threadIdx.x >> 5), nw = gridDim.x * kLoopWarps;
+    const int G = gridDim.x;
     const int64_t cap = a.cap;
+    // short factors: several warps of one CTA share a row (wpr warps per
+    // row, the largest power of two that still gives every row a group in
+    // one round), their partial sums added in warp order through shared
+    // memory -- fewer dependent load batches per row when rows are few
+    int wpr = 1;
+    while (wpr < kLoopWarps && (int64_t)(kLoopWarps / (2 * wpr)) * G >= n) wpr *= 2;
+    if (wpr > 1) {
+      const int warp = threadIdx.x >> 5, grp = warp / wpr, sub = warp % wpr;
+      const int v = grp * G + (int)blockIdx.x;  // rows interleaved over the CTAs
+      double acc = 0.0;
+      if (v < n) {
+        const double* av = A + (kCols ? col_off(v, cap) : tri_off(v));
+        const int len = kCols ? n - v : v + 1;
+        const int stride = wpr * kWarp;
+        for (int j0 = sub * kWarp; j0 < len; j0 += 8 * stride) {
+          double aa[8], xx[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int j = j0 + u * stride + lane;
+            aa[u] = j < len ? __ldcg(av + j) : 0.0;
+            xx[u] = j < len ? xload(v, j) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc = fma(aa[u], xx[u], acc);
+        }
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) sh.gred[warp] = acc;
+      __syncthreads();
+      if (v < n && sub == 0 && lane == 0) {
+        double t = sh.gred[grp * wpr];
+        for (int h = 1; h < wpr; ++h) t += sh.gred[grp * wpr + h];
+        finish(v, t);
+      }
+      __syncthreads();
+      return;
+    }
+    const int gw = blockIdx.x * kLoopWarps + (threadIdx.x >> 5), nw = G * kLoopWarps;
     for (int v = gw; v < n; v += nw) {
       const double* av = A + (kCols ? col_off(v, cap) : tri_off(v));
       const int len = kCols ? n - v : v + 1;
