@@ -43,6 +43,7 @@ namespace rbf {
 
 constexpr int kLoopThreads = 512;
 constexpr int kLoopWarps = kLoopThreads / 32;
+static_assert(kLoopThreads == 512, "scan prologues shift by log2(kLoopThreads) = 9");
 constexpr int kClusterCTAs = 16;
 constexpr int kSupTile = 2048;       // GlobalPath: supports staged per scan tile
 constexpr int kRowSmemMax = 8192;    // GlobalPath: row held in shared memory
@@ -1351,8 +1352,11 @@ struct MsgPath {
   // targets per lane chosen so the CTA's rows fill as many warps as possible
   __device__ __forceinline__ void scan(const int* gpos, const double* gpt, const double* gdisp, int card, int n,
                        int par) {
-    const int lo = (int)((int64_t)card * blockIdx.x / gridDim.x);
-    const int hi = (int)((int64_t)card * (blockIdx.x + 1) / gridDim.x);
+    // this CTA's rows [lo, hi): shifts for the one-cluster team (no integer
+    // divisions in the scan prologue, which every warp executes)
+    const unsigned b = blockIdx.x, G = gridDim.x;
+    const int lo = G == kClusterCTAs ? (int)(((unsigned)card * b) >> 4) : (int)((int64_t)card * b / G);
+    const int hi = G == kClusterCTAs ? (int)(((unsigned)card * (b + 1)) >> 4) : (int)((int64_t)card * (b + 1) / G);
     const int mine = hi - lo;
     if (mine <= kLoopWarps)
       scan_t<1>(gpos, gpt, gdisp, lo, hi, n, par);
@@ -1369,14 +1373,15 @@ struct MsgPath {
                          int par) {
     const int tid = threadIdx.x, lane = tid & 31;
     const int tgroups = (hi - lo + kTPT - 1) / kTPT;
-    int S = 32;
-    while (S > 1 && tgroups * S > kLoopThreads) S >>= 1;
-    const int per_round = kLoopThreads / S;
-    const int rounds = (tgroups + per_round - 1) / per_round;
-    const int sub = tid % S;
+    int lg = 5;  // S = 1 << lg lanes per target group: shifts and masks only
+    while (lg > 0 && (tgroups << lg) > kLoopThreads) --lg;
+    const int S = 1 << lg;
+    const int per_round = kLoopThreads >> lg;
+    const int rounds = (tgroups + per_round - 1) >> (9 - lg);  // kLoopThreads = 2^9
+    const int sub = tid & (S - 1);
     Best bu{-1.0, kNone}, br{-1.0, kNone};
     for (int rd = 0; rd < rounds; ++rd) {
-      const int tg = rd * per_round + tid / S;
+      const int tg = rd * per_round + (tid >> lg);
       double px[kTPT], py[kTPT], pz[kTPT];
       double v[16];
 #pragma unroll
