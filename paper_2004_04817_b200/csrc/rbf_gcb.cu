@@ -324,8 +324,11 @@ struct GlobalPath {
   __device__ __forceinline__ void scan(const int* gpos, const double* gpt, const double* gdisp, int card,
                                        int n, int par) {
     const int tid = threadIdx.x, G = gridDim.x;
-    const int lo = (int)((int64_t)card * blockIdx.x / G);
-    const int hi = (int)((int64_t)card * (blockIdx.x + 1) / G);
+    // 32-bit division when card * G fits (Nb <= 2^31 / 148): cheaper than 64-bit in every warp
+    const bool narrow = (int64_t)card * G < (1ll << 31);
+    const int lo = narrow ? (int)((unsigned)(card * blockIdx.x) / (unsigned)G) : (int)((int64_t)card * blockIdx.x / G);
+    const int hi = narrow ? (int)((unsigned)(card * (blockIdx.x + 1)) / (unsigned)G)
+                          : (int)((int64_t)card * (blockIdx.x + 1) / G);
     const double* gx = a.sup;
     const int cap = a.cap;
     // tail-round operands in the (idle) row buffer
@@ -1859,6 +1862,8 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
     t2_carry = 0.0;
   }
 
+  const int card_max = (a.nb + m - 1) / m;
+  int gk = k % m;
   while (!done_loop) {
     if (n >= a.max_supports) {
       done_loop = 1;
@@ -1867,12 +1872,12 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
     // one-cluster paths hand over to the whole-GPU grid once a group scan
     // (card x n pairs on 16 SMs) costs more than the grid's extra barriers
     if (self_mode != RBF_GCB_GRID && self_mode != RBF_GCB_CLUSTER &&
-        (int64_t)((a.nb + m - 1) / m) * n > kClusterScanPairs) {
+        (int64_t)card_max * n > kClusterScanPairs) {
       save(RBF_EGROW, RBF_GCB_GRID);
       return;
     }
     if (n >= Path::kMaxN - 1) {  // beyond this path's resident capacity
-      const bool big_scans = (int64_t)((a.nb + m - 1) / m) * n > kSmemScanPairs;
+      const bool big_scans = (int64_t)card_max * n > kSmemScanPairs;
       save(RBF_EGROW, self_mode == RBF_GCB_MSG ? (big_scans ? RBF_GCB_GRID : RBF_GCB_SMEM)
                       : self_mode == RBF_GCB_SMEM ? RBF_GCB_CLUSTER : self_mode);
       return;
@@ -1882,7 +1887,7 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
       return;
     }
     const uint64_t t_a = leader_timer();
-    const int gi = k % m;
+    const int gi = gk;  // == k % m, advanced with k (no division per iteration)
     const int off = P.group_off(gi);
     const int card = P.group_off(gi + 1) - off;
     const int* gpos = a.group_pos + off;
@@ -1947,6 +1952,7 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
       streak_ok = 0;
     }
     k += 1;
+    gk = gk + 1 == m ? 0 : gk + 1;
   }
 
   // final verification sweep (selection.py:388-412), natural order
