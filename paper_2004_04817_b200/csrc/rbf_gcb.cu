@@ -45,6 +45,7 @@ constexpr int kLoopThreads = 512;
 constexpr int kLoopWarps = kLoopThreads / 32;
 static_assert(kLoopThreads == 512, "scan prologues shift by log2(kLoopThreads) = 9");
 constexpr int kClusterCTAs = 16;
+static_assert(kClusterCTAs == 16, "one-cluster scans split rows with >> 4");
 constexpr int kSupTile = 2048;       // GlobalPath: supports staged per scan tile
 constexpr int kRowSmemMax = 8192;    // GlobalPath: row held in shared memory
 constexpr int kSmallMax = 1024;      // SmemPath: supports resident in shared memory
@@ -405,10 +406,11 @@ struct GlobalPath {
                                              Stage& stage, FinishRow& finish_row) {
     const int tid = threadIdx.x;
     const int groups = (rem + kT - 1) / kT;
-    int S = 32;
-    while (S > 1 && groups * S > kLoopThreads) S >>= 1;
-    while (S > 1 && (S >> 1) >= n) S >>= 1;
-    const int g = tid / S, sub = tid % S;
+    int lg = 5;  // S = 2^lg lanes per group: shifts and masks, no divisions
+    while (lg > 0 && (groups << lg) > kLoopThreads) --lg;
+    while (lg > 0 && (1 << (lg - 1)) >= n) --lg;
+    const int S = 1 << lg;
+    const int g = tid >> lg, sub = tid & (S - 1);
     const bool active = g < groups;
     if (tid < rem) {  // prefetch row tid's epilogue operands
       const int tt = t0 + tid;
@@ -815,17 +817,18 @@ struct SmemPath {
   __device__ __forceinline__ void scan(const int* gpos, const double* gpt, const double* gdisp, int card, int n,
                        int par) {
     const int tid = threadIdx.x, lane = tid & 31;
-    const int lo = (int)((int64_t)card * blockIdx.x / kClusterCTAs);
-    const int hi = (int)((int64_t)card * (blockIdx.x + 1) / kClusterCTAs);
+    const int lo = (int)(((unsigned)card * blockIdx.x) >> 4);  // kClusterCTAs = 16
+    const int hi = (int)(((unsigned)card * (blockIdx.x + 1)) >> 4);
     const int tgroups = (hi - lo + kTPT - 1) / kTPT;
-    int S = 32;
-    while (S > 1 && tgroups * S > kLoopThreads) S >>= 1;
-    const int per_round = kLoopThreads / S;
-    const int rounds = (tgroups + per_round - 1) / per_round;
-    const int sub = tid % S;
+    int lg = 5;  // S = 2^lg lanes per target group: shifts and masks only
+    while (lg > 0 && (tgroups << lg) > kLoopThreads) --lg;
+    const int S = 1 << lg;
+    const int per_round = kLoopThreads >> lg;
+    const int rounds = (tgroups + per_round - 1) >> (9 - lg);  // kLoopThreads = 2^9
+    const int sub = tid & (S - 1);
     Best bu{-1.0, kNone}, br{-1.0, kNone};
     for (int rd = 0; rd < rounds; ++rd) {
-      const int tg = rd * per_round + tid / S;
+      const int tg = rd * per_round + (tid >> lg);
       double px[kTPT], py[kTPT], pz[kTPT];
       double v[16];
 #pragma unroll
