@@ -1221,13 +1221,16 @@ struct MsgPath {
     unsigned done = 0, spins = 0;
     uint64_t t0 = 0;
     while (true) {
+      // suspend-time hint: the warp sleeps in the barrier unit (up to 1 ms)
+      // instead of re-issuing try_wait -- spinning warps were ~15 % of the
+      // kernel's issued instructions, taken from the warps doing the work
       asm volatile(
-          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
           : "=r"(done)
-          : "r"(addr), "r"(parity)
+          : "r"(addr), "r"(parity), "r"(1000000u)
           : "memory");
       if (done) break;
-      if ((++spins & 4095u) == 0) {
+      if ((++spins & 63u) == 0) {
         const uint64_t now = globaltimer_ns();
         if (t0 == 0) {
           t0 = now;
