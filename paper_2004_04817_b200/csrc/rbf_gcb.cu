@@ -609,9 +609,10 @@ struct GlobalPath {
       return kRejectPivot;
     }
     const double l = sqrt(pivot2);
-    const double yn0 = (__ldg(a.disp + 3 * (int64_t)pos) - cm.dbl[2]) / l;
-    const double yn1 = (__ldg(a.disp + 3 * (int64_t)pos + 1) - cm.dbl[3]) / l;
-    const double yn2 = (__ldg(a.disp + 3 * (int64_t)pos + 2) - cm.dbl[4]) / l;
+    const double inv_l = 1.0 / l;  // one division; every later 1/l is a multiply
+    const double yn0 = (__ldg(a.disp + 3 * (int64_t)pos) - cm.dbl[2]) * inv_l;
+    const double yn1 = (__ldg(a.disp + 3 * (int64_t)pos + 1) - cm.dbl[3]) * inv_l;
+    const double yn2 = (__ldg(a.disp + 3 * (int64_t)pos + 2) - cm.dbl[4]) * inv_l;
     double* Lrow = a.L + tri_off(n);
     double* Lirow = a.Li + tri_off(n);
     double* wgt = a.sup + 3 * (int64_t)cap;
@@ -620,7 +621,7 @@ struct GlobalPath {
     const int nn = n;
     xs = stage_x(s.c1, n);
     tri_gemv<true>(s.lic, n, [&](int v, int e) { return xs ? xs[v + e] : __ldcg(s.c1 + v + e); }, [&](int j, double u) {
-      const double lij = -u / l;
+      const double lij = -u * inv_l;
       Lirow[j] = lij;
       s.lic[col_off(j, cap) + (nn - j)] = lij;
       Lrow[j] = __ldcg(s.c1 + j);
@@ -629,8 +630,8 @@ struct GlobalPath {
       wgt[2 * cap + j] = fma(lij, yn2, __ldcg(wgt + 2 * cap + j));
     });
     if (blockIdx.x == 0 && tid == 0) {
-      Lirow[n] = 1.0 / l;
-      s.lic[col_off(n, cap)] = 1.0 / l;
+      Lirow[n] = inv_l;
+      s.lic[col_off(n, cap)] = inv_l;
       Lrow[n] = l;
       a.y[3 * (int64_t)n] = yn0;
       a.y[3 * (int64_t)n + 1] = yn1;
@@ -638,9 +639,9 @@ struct GlobalPath {
       a.sup[n] = px;
       a.sup[cap + n] = py;
       a.sup[2 * cap + n] = pz;
-      wgt[n] = yn0 / l;
-      wgt[cap + n] = yn1 / l;
-      wgt[2 * cap + n] = yn2 / l;
+      wgt[n] = yn0 * inv_l;
+      wgt[cap + n] = yn1 * inv_l;
+      wgt[2 * cap + n] = yn2 * inv_l;
       a.sel[n] = pos;
     }
     if (tid == 0) a.inel[pos] = 1;
@@ -1018,9 +1019,10 @@ struct SmemPath {
       return kRejectPivot;
     }
     const double l = sqrt(pivot2);
-    const double yn0 = (__ldg(a.disp + 3 * (int64_t)pos) - cm.dbl[2]) / l;
-    const double yn1 = (__ldg(a.disp + 3 * (int64_t)pos + 1) - cm.dbl[3]) / l;
-    const double yn2 = (__ldg(a.disp + 3 * (int64_t)pos + 2) - cm.dbl[4]) / l;
+    const double inv_l = 1.0 / l;  // one division; every later 1/l is a multiply
+    const double yn0 = (__ldg(a.disp + 3 * (int64_t)pos) - cm.dbl[2]) * inv_l;
+    const double yn1 = (__ldg(a.disp + 3 * (int64_t)pos + 1) - cm.dbl[3]) * inv_l;
+    const double yn2 = (__ldg(a.disp + 3 * (int64_t)pos + 2) - cm.dbl[4]) * inv_l;
     // column partials of u = Li^T c, v = Li^T y over this CTA's own rows:
     // warp w owns 32-column chunks J = w, w + 16, ...; every load of a chunk
     // is issued before its FMAs
@@ -1079,7 +1081,7 @@ struct SmemPath {
     double* wgt = a.sup + 3 * (int64_t)cap;
     for (int e = tid; e < (jhi - jlo) * kClusterCTAs; e += kLoopThreads) {
       const int jj = e / kClusterCTAs, q = e % kClusterCTAs, j = jlo + jj;
-      const double lij = -cm.red[4 * jj] / l;
+      const double lij = -cm.red[4 * jj] * inv_l;
       const double w0 = fma(lij, yn0, cm.red[4 * jj + 1]);
       const double w1 = fma(lij, yn1, cm.red[4 * jj + 2]);
       const double w2 = fma(lij, yn2, cm.red[4 * jj + 3]);
@@ -1100,15 +1102,15 @@ struct SmemPath {
       sh.sx[n] = px * inv_r;
       sh.sy[n] = py * inv_r;
       sh.sz[n] = pz * inv_r;
-      sh.wx[n] = yn0 / l;
-      sh.wy[n] = yn1 / l;
-      sh.wz[n] = yn2 / l;
+      sh.wx[n] = yn0 * inv_l;
+      sh.wy[n] = yn1 * inv_l;
+      sh.wz[n] = yn2 * inv_l;
       sh.y0[n] = yn0;
       sh.y1[n] = yn1;
       sh.y2[n] = yn2;
       a.inel[pos] = 1;
       if (rank == 0) {  // and in the global state
-        Lirow[n] = 1.0 / l;
+        Lirow[n] = inv_l;
         a.L[tri_off(n) + n] = l;
         a.y[3 * (int64_t)n] = yn0;
         a.y[3 * (int64_t)n + 1] = yn1;
@@ -1116,9 +1118,9 @@ struct SmemPath {
         a.sup[n] = px;
         a.sup[cap + n] = py;
         a.sup[2 * cap + n] = pz;
-        wgt[n] = yn0 / l;
-        wgt[cap + n] = yn1 / l;
-        wgt[2 * cap + n] = yn2 / l;
+        wgt[n] = yn0 * inv_l;
+        wgt[cap + n] = yn1 * inv_l;
+        wgt[2 * cap + n] = yn2 * inv_l;
         a.sel[n] = pos;
       }
     }
@@ -1664,7 +1666,7 @@ struct MsgPath {
         if (lane == 0) sh.Licol[own_col_off(qb, rk) + (n - jb)] = ub * neg_inv_l;
       }
     }
-    if (n % kClusterCTAs == rk && tid == 0) sh.Licol[own_col_off(n / kClusterCTAs, rk)] = 1.0 / l;
+    if (n % kClusterCTAs == rk && tid == 0) sh.Licol[own_col_off(n / kClusterCTAs, rk)] = inv_l;
     pc.mark(15);
     const int owner = n % kClusterCTAs, qn = n / kClusterCTAs;
     double* Lirow_g = a.Li + tri_off(n);
@@ -1688,11 +1690,11 @@ struct MsgPath {
         a.sup[n] = px;
         a.sup[cap + n] = py;
         a.sup[2 * cap + n] = pz;
-        wgt[n] = yn0 / l;
-        wgt[cap + n] = yn1 / l;
-        wgt[2 * cap + n] = yn2 / l;
+        wgt[n] = yn0 * inv_l;
+        wgt[cap + n] = yn1 * inv_l;
+        wgt[2 * cap + n] = yn2 * inv_l;
         a.sel[n] = pos;
-        Lirow_g[n] = 1.0 / l;
+        Lirow_g[n] = inv_l;
         a.L[tri_off(n) + n] = l;
       }
     }
@@ -1705,7 +1707,7 @@ struct MsgPath {
       }
       if (tid == 0) {
         sh.Lown[o + n] = l;
-        sh.Liown[o + n] = 1.0 / l;
+        sh.Liown[o + n] = inv_l;
       }
     }
     wait(kMbW);
@@ -1723,9 +1725,9 @@ struct MsgPath {
       }
     }
     if (tid == 0) {
-      sh.wx[n] = yn0 / l;
-      sh.wy[n] = yn1 / l;
-      sh.wz[n] = yn2 / l;
+      sh.wx[n] = yn0 * inv_l;
+      sh.wy[n] = yn1 * inv_l;
+      sh.wz[n] = yn2 * inv_l;
     }
     n += 1;
     __syncthreads();
