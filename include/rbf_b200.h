@@ -194,8 +194,11 @@ typedef struct rbf_gcb_state {
   double phase_cycles[16];
 } rbf_gcb_state;
 
+/* rbf_gcb_args.flags */
+#define RBF_GCB_PHASES 1
+
 /* Launch shapes of the selection kernel:
- *  MSG     one 16-CTA cluster, n < 448: the factor rows (owner-stable, row
+ *  MSG     one 16-CTA cluster, n < 384: the factor rows (owner-stable, row
  *          i in CTA i % 16) and all vectors resident in shared memory; every
  *          cross-CTA value is pushed with st.async into the consumer's
  *          mbarrier -- no cluster barriers in steady state;
@@ -221,7 +224,8 @@ typedef struct rbf_gcb_args {
   int32_t clusters;         /* MSG path: 16-CTA clusters sharing the group
                                scans (0 = library default); each computes the
                                appends redundantly, scan partials meet in L2 */
-  int32_t reserved;
+  int32_t flags;            /* RBF_GCB_PHASES: record per-phase SM cycles (costs
+                               ~4 % of the loop; off by default)              */
   double radius, tol;
   double dup_dist;          /* NEAR_DUPLICATE_FRACTION * radius            */
   /* factor state (device), capacity in rows */

@@ -22,6 +22,7 @@ RBF_ENCCL = 4
 RBF_EGROW = 5
 RBF_ESTALL = 6
 RBF_EPARSE = 7
+GCB_PHASES = 1  # rbf_gcb_args.flags: record per-phase SM cycles
 STATUS_DONE = 1
 GCB_AUTO = 0
 GCB_CLUSTER = 1
@@ -89,7 +90,7 @@ class GcbArgs(ctypes.Structure):
         ("mode", ctypes.c_int32),
         ("max_supports", ctypes.c_int32),
         ("clusters", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
         ("radius", ctypes.c_double),
         ("tol", ctypes.c_double),
         ("dup_dist", ctypes.c_double),

@@ -148,27 +148,28 @@ struct GridTeam {
 
 // CTA 0's SM clock at phase boundaries (diagnostics in rbf_gcb_state),
 // kept by thread 0 of CTA 0 in shared memory.
-struct PhaseClock {
-  double* acc;
+template <bool kOn>
+struct PhaseClockT {  // kOn = false compiles every mark away (the clock reads are
+  double* acc;        // volatile and cost ~4 % of the loop as scheduling fences)
   long long last;
   bool on;
   __device__ __forceinline__ void start(double* smem_acc) {
     acc = smem_acc;
-    on = blockIdx.x == 0 && threadIdx.x == 0;
-    if (on) {
+    on = kOn && blockIdx.x == 0 && threadIdx.x == 0;
+    if (kOn && on) {
       for (int i = 0; i < 16; ++i) acc[i] = 0.0;
       last = clock64();
     }
   }
   __device__ __forceinline__ void mark(int phase) {
-    if (on) {
+    if (kOn && on) {
       const long long now = clock64();
       acc[phase] += (double)(now - last);
       last = now;
     }
   }
   __device__ __forceinline__ void count(int slot) {
-    if (on) acc[slot] += 1.0;
+    if (kOn && on) acc[slot] += 1.0;
   }
 };
 
@@ -258,14 +259,14 @@ struct GlobalShared {
   double gred[kLoopWarps];  // row products: per-warp partials of a shared row
 };
 
-template <class Team>
+template <class Team, class Clock>
 struct GlobalPath {
   const rbf_gcb_args& a;
   const LoopScratch& s;
   GlobalShared& sh;
   Team team;
   double inv_r;
-  PhaseClock& pc;
+  Clock& pc;
 
   static constexpr int kMaxN = kRowSmemMax;
   __device__ Common& cm() { return sh.cm; }
@@ -755,12 +756,13 @@ __device__ __forceinline__ void row_dot_pair(const double* ra, int len_a, const 
   sb = warp_sum(acc_b);
 }
 
+template <class Clock>
 struct SmemPath {
   const rbf_gcb_args& a;
   const LoopScratch& s;
   SmemShared& sh;
   double inv_r;
-  PhaseClock& pc;
+  Clock& pc;
 
   static constexpr int kMaxN = kSmallMax;
   static constexpr int kTPT = 4;  // targets per lane in group scans
@@ -1189,12 +1191,13 @@ __device__ __forceinline__ void st_async2(unsigned raddr, double v0, double v1, 
                : "memory");
 }
 
+template <class Clock>
 struct MsgPath {
   const rbf_gcb_args& a;
   const LoopScratch& s;
   MsgShared& sh;
   double inv_r;
-  PhaseClock& pc;
+  Clock& pc;
   unsigned phase_bits;  // parity of the next completion of each mbarrier
 
   static constexpr int kMaxN = kMsgMax;
@@ -1806,8 +1809,8 @@ __device__ void device_seeds(Path& P, const rbf_gcb_args& a, const LoopScratch& 
   }
 }
 
-template <class Path>
-__device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s, PhaseClock& pc,
+template <class Path, class Clock>
+__device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s, Clock& pc,
                            int self_mode) {
   const int tid = threadIdx.x;
   const bool leader = blockIdx.x == 0 && tid == 0;
@@ -1995,37 +1998,42 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
 
 extern __shared__ __align__(16) unsigned char g_smem[];
 
-template <class Team>
+template <class Team, bool kPh>
 __device__ void run_global(const rbf_gcb_args& a, const LoopScratch& s, Team team, int mode) {
   GlobalShared& sh = *reinterpret_cast<GlobalShared*>(g_smem);
-  PhaseClock pc;
+  PhaseClockT<kPh> pc;
   pc.start(sh.cm.phase);
-  GlobalPath<Team> P{a, s, sh, team, 1.0 / a.radius, pc};
+  GlobalPath<Team, PhaseClockT<kPh>> P{a, s, sh, team, 1.0 / a.radius, pc};
   gcb_driver(P, a, s, pc, mode);
 }
 
+// kPh: with the per-phase clock (rbf_gcb_args.flags & RBF_GCB_PHASES)
+template <bool kPh>
 __global__ void __launch_bounds__(kLoopThreads, 1) gcb_cluster_kernel(rbf_gcb_args a, LoopScratch s) {
-  run_global(a, s, ClusterTeam{}, RBF_GCB_CLUSTER);
+  run_global<ClusterTeam, kPh>(a, s, ClusterTeam{}, RBF_GCB_CLUSTER);
 }
 
+template <bool kPh>
 __global__ void __launch_bounds__(kLoopThreads, 1) gcb_grid_kernel(rbf_gcb_args a, LoopScratch s) {
-  run_global(a, s, GridTeam{s.bar, s.fault}, RBF_GCB_GRID);
+  run_global<GridTeam, kPh>(a, s, GridTeam{s.bar, s.fault}, RBF_GCB_GRID);
 }
 
+template <bool kPh>
 __global__ void __launch_bounds__(kLoopThreads, 1) gcb_smem_kernel(rbf_gcb_args a, LoopScratch s) {
   SmemShared& sh = *reinterpret_cast<SmemShared*>(g_smem);
-  PhaseClock pc;
+  PhaseClockT<kPh> pc;
   pc.start(sh.cm.phase);
-  SmemPath P{a, s, sh, 1.0 / a.radius, pc};
+  SmemPath<PhaseClockT<kPh>> P{a, s, sh, 1.0 / a.radius, pc};
   gcb_driver(P, a, s, pc, RBF_GCB_SMEM);
   P.finish();
 }
 
+template <bool kPh>
 __global__ void __launch_bounds__(kLoopThreads, 1) gcb_msg_kernel(rbf_gcb_args a, LoopScratch s) {
   MsgShared& sh = *reinterpret_cast<MsgShared*>(g_smem);
-  PhaseClock pc;
+  PhaseClockT<kPh> pc;
   pc.start(sh.cm.phase);
-  MsgPath P{a, s, sh, 1.0 / a.radius, pc, 0u, 0u};
+  MsgPath<PhaseClockT<kPh>> P{a, s, sh, 1.0 / a.radius, pc, 0u, 0u};
   gcb_driver(P, a, s, pc, RBF_GCB_MSG);
   P.finish();
 }
@@ -2131,6 +2139,7 @@ extern "C" int rbf_gcb_run(const rbf_gcb_args* args, void* stream) {
   cudaStream_t st = as_stream(stream);
   RBF_CUDA_TRY(cudaMemsetAsync(s.bar, 0, 64, st));
   rbf_gcb_args acopy = a;
+  const bool ph = (a.flags & RBF_GCB_PHASES) != 0;
   if (mode == RBF_GCB_MSG) {
     int dev = 0;
     RBF_CUDA_TRY(cudaGetDevice(&dev));
@@ -2138,14 +2147,18 @@ extern "C" int rbf_gcb_run(const rbf_gcb_args* args, void* stream) {
     int ncl = a.clusters > 0 ? a.clusters : kMsgDefaultClusters;
     ncl = ncl < 1 ? 1 : (ncl > max_cl ? max_cl : (ncl > 16 ? 16 : ncl));
     RBF_CUDA_TRY(cudaMemsetAsync(s.xseq, 0, sizeof(unsigned) * 2 * 16, st));
-    RBF_CUDA_TRY(launch_cluster((const void*)gcb_msg_kernel, acopy, s, sizeof(MsgShared), st, ncl));
+    RBF_CUDA_TRY(launch_cluster(ph ? (const void*)gcb_msg_kernel<true> : (const void*)gcb_msg_kernel<false>,
+                                acopy, s, sizeof(MsgShared), st, ncl));
   } else if (mode == RBF_GCB_SMEM) {
-    RBF_CUDA_TRY(launch_cluster((const void*)gcb_smem_kernel, acopy, s, sizeof(SmemShared), st));
+    RBF_CUDA_TRY(launch_cluster(ph ? (const void*)gcb_smem_kernel<true> : (const void*)gcb_smem_kernel<false>,
+                                acopy, s, sizeof(SmemShared), st));
   } else if (mode == RBF_GCB_CLUSTER) {
-    RBF_CUDA_TRY(launch_cluster((const void*)gcb_cluster_kernel, acopy, s, sizeof(GlobalShared), st));
+    RBF_CUDA_TRY(launch_cluster(ph ? (const void*)gcb_cluster_kernel<true> : (const void*)gcb_cluster_kernel<false>,
+                                acopy, s, sizeof(GlobalShared), st));
   } else {
     const size_t smem = sizeof(GlobalShared);
-    RBF_CUDA_TRY(cudaFuncSetAttribute(gcb_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto grid_kernel = ph ? gcb_grid_kernel<true> : gcb_grid_kernel<false>;
+    RBF_CUDA_TRY(cudaFuncSetAttribute(grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // Li is read twice per append (c0 = Li row, c = c0 + Li r): keep its first
     // persisting-L2 share resident (an access-policy window on this launch),
     // while L and the column copy stream from HBM. rbf_l2_release() returns
@@ -2172,7 +2185,7 @@ extern "C" int rbf_gcb_run(const rbf_gcb_args* args, void* stream) {
     cfg.stream = st;
     cfg.attrs = attrs;
     cfg.numAttrs = nattr;
-    RBF_CUDA_TRY(cudaLaunchKernelEx(&cfg, gcb_grid_kernel, acopy, s));
+    RBF_CUDA_TRY(cudaLaunchKernelEx(&cfg, grid_kernel, acopy, s));
   }
   return RBF_OK;
 }

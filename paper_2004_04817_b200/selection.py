@@ -504,7 +504,7 @@ def gcb_select(boundary, config):
     return _gcb_run(boundary, config)
 
 
-def _gcb_run(boundary, config, mode=None):
+def _gcb_run(boundary, config, mode=None, phases=None):
     nb = len(boundary)
     m = config.m
     if not 1 <= m <= nb:
@@ -540,6 +540,9 @@ def _gcb_run(boundary, config, mode=None):
     import os
 
     args.clusters = int(os.environ.get("RBF_GCB_CLUSTERS", "0"))
+    if phases is None:  # RBF_GCB_PHASES=1: per-phase device cycles in history.device_phase_cycles
+        phases = os.environ.get("RBF_GCB_PHASES", "") == "1"
+    args.flags = N.GCB_PHASES if phases else 0
     args.radius = radius
     args.tol = float(config.tol)
     args.dup_dist = NEAR_DUPLICATE_FRACTION * config.radius
@@ -620,7 +623,7 @@ def _gcb_run(boundary, config, mode=None):
         t2_s=float(fin["t2_s"]),
     )
     # diagnostics: SM cycles of CTA 0 per phase of the device loop
-    history.device_phase_cycles = dict(zip(N.PHASES, list(st.phase_cycles)))
+    history.device_phase_cycles = dict(zip(N.PHASES, list(st.phase_cycles))) if phases else {}
     history.device_mode = {N.GCB_CLUSTER: "cluster", N.GCB_GRID: "grid", N.GCB_SMEM: "smem",
                            N.GCB_MSG: "msg"}[args.mode]
     support = SupportSet(nodes=idx[sel], points=boundary.points[sel], weights=weights)

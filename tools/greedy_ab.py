@@ -1,6 +1,7 @@
 """A/B helper: one warm gcb_select per m on the configs[2] boundary (Nb = 80k);
 prints device time, t1/t2 sums, the device phase split and a sequence hash."""
 import os, sys, time, json, numpy as np, torch
+os.environ.setdefault("RBF_GCB_PHASES", "1")  # phase split (the clock costs ~4 % of the loop)
 sys.path.insert(0, ".")
 import paper_2004_04817_b200 as P
 from paper_2004_04817_b200 import _native as N, workloads as W
