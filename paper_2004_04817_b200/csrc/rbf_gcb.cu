@@ -477,8 +477,10 @@ struct GlobalPath {
   // column-packed copy (vector j = rows j..n-1, x index j + e); one warp per
   // vector, vectors strided over every warp of the team, 16 loads per lane
   // in flight once the factor is long. finish(v, sum) runs on lane 0.
-  template <bool kCols, class XL, class Fin>
-  __device__ __forceinline__ void tri_gemv(const double* A, int n, XL xload, Fin finish) {
+  // pre(v) -> double4: the finishing lane's operands of vector v, loaded
+  // before the dot product so their L2 latency overlaps it
+  template <bool kCols, class XL, class Pre, class Fin>
+  __device__ __forceinline__ void tri_gemv(const double* A, int n, XL xload, Pre pre, Fin finish) {
     const int lane = threadIdx.x & 31;
     const int G = gridDim.x;
     const int64_t cap = a.cap;
@@ -492,6 +494,7 @@ struct GlobalPath {
       const int warp = threadIdx.x >> 5, grp = warp / wpr, sub = warp % wpr;
       const int v = grp * G + (int)blockIdx.x;  // rows interleaved over the CTAs
       double acc = 0.0;
+      const double4 pf = (v < n && sub == 0 && lane == 0) ? pre(v) : make_double4(0.0, 0.0, 0.0, 0.0);
       if (v < n) {
         const double* av = A + (kCols ? col_off(v, cap) : tri_off(v));
         const int len = kCols ? n - v : v + 1;
@@ -514,7 +517,7 @@ struct GlobalPath {
       if (v < n && sub == 0 && lane == 0) {
         double t = sh.gred[grp * wpr];
         for (int h = 1; h < wpr; ++h) t += sh.gred[grp * wpr + h];
-        finish(v, t);
+        finish(v, t, pf);
       }
       __syncthreads();
       return;
@@ -524,8 +527,9 @@ struct GlobalPath {
       const double* av = A + (kCols ? col_off(v, cap) : tri_off(v));
       const int len = kCols ? n - v : v + 1;
       auto xl = [&](int e) { return xload(v, e); };
+      const double4 pf = lane == 0 ? pre(v) : make_double4(0.0, 0.0, 0.0, 0.0);
       const double acc = len > 1024 ? row_dot<16>(av, len, xl, lane) : row_dot<8>(av, len, xl, lane);
-      if (lane == 0) finish(v, acc);
+      if (lane == 0) finish(v, acc, pf);
     }
   }
 
@@ -554,28 +558,36 @@ struct GlobalPath {
     if (check_dup && n > 0 && near) return kRejectDup;
     pc.mark(1);
     // c0 = Li row
-    tri_gemv<false>(a.Li, n, [&](int, int e) { return row[e]; },
-                    [&](int v, double acc) { s.c0[v] = acc; });
+    auto no_pre = [](int) { return make_double4(0.0, 0.0, 0.0, 0.0); };
+    tri_gemv<false>(a.Li, n, [&](int, int e) { return row[e]; }, no_pre,
+                    [&](int v, double acc, const double4&) { s.c0[v] = acc; });
     team.sync();
     pc.mark(2);
     // r = row - L c0
     const double* xs = stage_x(s.c0, n);
     tri_gemv<false>(a.L, n, [&](int, int e) { return xs ? xs[e] : __ldcg(s.c0 + e); },
-                    [&](int v, double acc) { s.r[v] = row[v] - acc; });
+                    no_pre,
+                    [&](int v, double acc, const double4&) { s.r[v] = row[v] - acc; });
     team.sync();
     pc.mark(3);
     // c = c0 + Li r, with this CTA's partials of c.c and c.y
     double pcc = 0.0, pcy0 = 0.0, pcy1 = 0.0, pcy2 = 0.0;
     __syncthreads();
     xs = stage_x(s.r, n);
-    tri_gemv<false>(a.Li, n, [&](int, int e) { return xs ? xs[e] : __ldcg(s.r + e); }, [&](int v, double acc) {
-      const double c = __ldcg(s.c0 + v) + acc;
-      s.c1[v] = c;
-      pcc = fma(c, c, pcc);
-      pcy0 = fma(c, __ldcg(a.y + 3 * (int64_t)v), pcy0);
-      pcy1 = fma(c, __ldcg(a.y + 3 * (int64_t)v + 1), pcy1);
-      pcy2 = fma(c, __ldcg(a.y + 3 * (int64_t)v + 2), pcy2);
-    });
+    tri_gemv<false>(
+        a.Li, n, [&](int, int e) { return xs ? xs[e] : __ldcg(s.r + e); },
+        [&](int v) {
+          return make_double4(__ldcg(s.c0 + v), __ldcg(a.y + 3 * (int64_t)v), __ldcg(a.y + 3 * (int64_t)v + 1),
+                              __ldcg(a.y + 3 * (int64_t)v + 2));
+        },
+        [&](int v, double acc, const double4& pf) {
+          const double c = pf.x + acc;
+          s.c1[v] = c;
+          pcc = fma(c, c, pcc);
+          pcy0 = fma(c, pf.y, pcy0);
+          pcy1 = fma(c, pf.z, pcy1);
+          pcy2 = fma(c, pf.w, pcy2);
+        });
     Common& cm = sh.cm;
     if (lane == 0) {
       cm.wred[warp][0] = pcc;
@@ -621,15 +633,21 @@ struct GlobalPath {
     // move by Li[n][j] y_n (w = Li^T y with the new row appended)
     const int nn = n;
     xs = stage_x(s.c1, n);
-    tri_gemv<true>(s.lic, n, [&](int v, int e) { return xs ? xs[v + e] : __ldcg(s.c1 + v + e); }, [&](int j, double u) {
-      const double lij = -u * inv_l;
-      Lirow[j] = lij;
-      s.lic[col_off(j, cap) + (nn - j)] = lij;
-      Lrow[j] = __ldcg(s.c1 + j);
-      wgt[j] = fma(lij, yn0, __ldcg(wgt + j));
-      wgt[cap + j] = fma(lij, yn1, __ldcg(wgt + cap + j));
-      wgt[2 * cap + j] = fma(lij, yn2, __ldcg(wgt + 2 * cap + j));
-    });
+    tri_gemv<true>(
+        s.lic, n, [&](int v, int e) { return xs ? xs[v + e] : __ldcg(s.c1 + v + e); },
+        [&](int j) {
+          return make_double4(__ldcg(s.c1 + j), __ldcg(wgt + j), __ldcg(wgt + cap + j),
+                              __ldcg(wgt + 2 * cap + j));
+        },
+        [&](int j, double u, const double4& pf) {
+          const double lij = -u * inv_l;
+          Lirow[j] = lij;
+          s.lic[col_off(j, cap) + (nn - j)] = lij;
+          Lrow[j] = pf.x;
+          wgt[j] = fma(lij, yn0, pf.y);
+          wgt[cap + j] = fma(lij, yn1, pf.z);
+          wgt[2 * cap + j] = fma(lij, yn2, pf.w);
+        });
     if (blockIdx.x == 0 && tid == 0) {
       Lirow[n] = inv_l;
       s.lic[col_off(n, cap)] = inv_l;
