@@ -1907,8 +1907,10 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
     }
     if (n >= Path::kMaxN - 1) {  // beyond this path's resident capacity
       const bool big_scans = (int64_t)card_max * n > kSmemScanPairs;
+      // past the shared-memory paths the factor passes need every SM's
+      // bandwidth: SMEM hands over to the grid (CLUSTER only when forced)
       save(RBF_EGROW, self_mode == RBF_GCB_MSG ? (big_scans ? RBF_GCB_GRID : RBF_GCB_SMEM)
-                      : self_mode == RBF_GCB_SMEM ? RBF_GCB_CLUSTER : self_mode);
+                      : self_mode == RBF_GCB_SMEM ? RBF_GCB_GRID : self_mode);
       return;
     }
     if (n >= a.cap || nrec >= a.rec_cap) {

@@ -497,3 +497,19 @@ def test_concurrent_selections_and_evaluations(cuda):
         assert np.array_equal(out[name].support.nodes, serial[name].support.nodes)
         assert np.array_equal(out[name].support.weights, serial[name].support.weights)
         assert np.array_equal(out[name + "_u"], ref_u)
+
+
+def test_mode_handover_chain_matches_grid(cuda):
+    """MSG -> SMEM -> GRID hand-overs (small groups, n past 1024) give the same
+    selection as running the whole loop in the grid shape."""
+    from paper_2004_04817_b200 import _native as N
+    from paper_2004_04817_b200.selection import _gcb_run
+
+    g = load_golden("switch_m8")  # Nb = 4000 boundary; m = 40 keeps group scans small
+    b = cuda.BoundarySet(np.arange(len(g["points"])), g["points"], g["disp"])
+    cfg = cuda.SelectionConfig(radius=0.25, tol=1e-7, max_supports=1300, m=40, seed=3)
+    auto = _gcb_run(b, cfg)
+    grid = _gcb_run(b, cfg, mode=N.GCB_GRID)
+    assert len(auto.support) > 1024
+    assert np.array_equal(auto.support.nodes, grid.support.nodes)
+    assert rel(auto.support.weights, grid.support.weights) <= 1e-9
