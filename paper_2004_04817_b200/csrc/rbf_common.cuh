@@ -47,16 +47,30 @@ __device__ __forceinline__ double clamp_nonneg(double t) {
   return __hiloint2double(hi & keep, lo & keep);
 }
 
+// t = 1 - eta from r2 = eta^2 in 5 FP64 instructions. y0 = MUFU.RSQ64H(r2)
+// has relative error up to 2^-20 (tools/pair_lab.cu, measured on B200), so
+// with eta0 = r2 y0 and e = 1 - r2 y0^2 = 1 - eta0 y0,
+//   eta = eta0 (1 - e)^(-1/2) = eta0 (1 + e (1/2 + 3e/8)) + O(e^3),
+// a third-order correction (truncation ~2^-62) written as two nested FMAs:
+// |t - (1 - sqrt(r2))| <= 2.8e-16 over r2 in [1e-10, 1.2] (pair_lab), the
+// same ulp-level error as the 6-instruction rsqrt refinement it replaces.
+__device__ __forceinline__ double t_from_r2(double r2) {
+  const double y0 = rsqrt_approx(r2);
+  const double eta0 = r2 * y0;
+  const double e = fma(-eta0, y0, 1.0);
+  const double p = fma(e, 0.375, 0.5);
+  const double w = fma(e, p, 1.0);
+  return fma(-eta0, w, 1.0);
+}
+
 // Throughput pair: target (px,py,pz) and support (sx,sy,sz) already scaled
 // by 1/R; accumulates w * phi(|p - s|) into (ax, ay, az).
 //
-// FP64-pipe budget per pair: 3 DADD (differences) + 3 (r^2) + 5 (rsqrt
-// refinement) + 2 (t = 1 - r2*y, q = 5 - 4t = 4 eta + 1) + 3 (t^2, t^4,
-// t^4 q) + 3 DFMA (accumulate) = 19. eta = sqrt(r2) is never formed:
-// y = rsqrt(r2) comes from MUFU.RSQ64H plus one third-order correction
-// (relative error ~2^-60), t = fma(-r2, y, 1). r2 below 1e-200 is lifted to
-// 1e-200 (eta = 1e-100 gives phi = 1 exactly, like eta = 0) so the rsqrt
-// never sees zero. The clamp t = max(t, 0) is integer-only.
+// FP64-pipe budget per pair: 3 DADD (differences) + 3 (r^2) + 5 (t = 1 - eta)
+// + 4 (q = 5 - 4t = 4 eta + 1, t^2, t^4, t^4 q) + 3 DFMA (accumulate) = 18.
+// t_from_r2() never forms sqrt(r2) separately; see there. r2 below 1e-200 is
+// lifted to 1e-200 (eta = 1e-100 gives phi = 1 exactly, like eta = 0) so the
+// rsqrt never sees zero. The clamp t = max(t, 0) is integer-only.
 __device__ __forceinline__ void pair_accum(double px, double py, double pz,
                                            double sx, double sy, double sz,
                                            double wx, double wy, double wz,
@@ -66,11 +80,7 @@ __device__ __forceinline__ void pair_accum(double px, double py, double pz,
   const int kTinyHi = 0x16687e92;  // high word of 1e-200
   const int hi = __double2hiint(r2);
   r2 = __hiloint2double(max(hi, kTinyHi), __double2loint(r2));
-  const double y0 = rsqrt_approx(r2);
-  const double e = fma(-r2, y0 * y0, 1.0);
-  const double p = fma(e, 0.375, 0.5);
-  const double y = fma(p, y0 * e, y0);
-  double t = clamp_nonneg(fma(-r2, y, 1.0));
+  double t = clamp_nonneg(t_from_r2(r2));
   const double q = fma(-4.0, t, 5.0);
   t = t * t;
   const double f = (t * t) * q;
@@ -83,7 +93,7 @@ __device__ __forceinline__ void pair_accum(double px, double py, double pz,
 // to an origin o (the first support) and scaled by 1/R; per target
 // P = |p'|^2, per support (-2 s', S = |s'|^2) are precomputed, so
 //   r^2 = (P + S) + p'.(-2 s')            (1 DADD + 3 DFMA instead of 6)
-// and the pair costs 17 FP64-pipe instructions. Absolute error of r^2 is
+// and the pair costs 16 FP64-pipe instructions. Absolute error of r^2 is
 // ~4u(|p'| + |s'|)^2 (u = 2^-53) and dphi/d(r^2) = -10(1 - eta)^3 is
 // bounded, so phi moves by < 1e-13 on these domains (displacements agree
 // with the reference to ~1e-12 relative; tests/test_gpu_parity.py). Negative
@@ -96,11 +106,7 @@ __device__ __forceinline__ void pair_accum_expanded(double px, double py, double
   const int kTinyHi = 0x16687e92;  // high word of 1e-200
   const int hi = __double2hiint(r2);
   r2 = __hiloint2double(max(hi, kTinyHi), __double2loint(r2));
-  const double y0 = rsqrt_approx(r2);
-  const double e = fma(-r2, y0 * y0, 1.0);
-  const double p = fma(e, 0.375, 0.5);
-  const double y = fma(p, y0 * e, y0);
-  double t = clamp_nonneg(fma(-r2, y, 1.0));
+  double t = clamp_nonneg(t_from_r2(r2));
   const double q = fma(-4.0, t, 5.0);
   t = t * t;
   const double f = (t * t) * q;

@@ -111,7 +111,7 @@ eval_kernel(const double* __restrict__ tpts, const double* __restrict__ tdisp,
   }
 }
 
-// Volume kernel in expanded form (pair_accum_expanded, 17 FP64 per pair).
+// Volume kernel in expanded form (pair_accum_expanded, 16 FP64 per pair).
 // Origin = the first support, so the result does not depend on how the
 // targets are sharded.
 template <int MODE, int NT, int TPT, int TILE, int MINB>
@@ -193,7 +193,8 @@ __global__ void best_reduce_kernel(const Best* __restrict__ partials, int n, dou
 // Launch variants of the volume kernel: 0 the expanded pair form (128
 // threads x 6 targets), 1-5 the difference form at several geometries
 // (threads, targets per thread, support tile, min resident blocks), 6 the
-// expanded form at 128 x 4. RBF_EVAL_VARIANT selects one for experiments
+// expanded form at 128 x 4, 7-8 the difference form at 64 x 6 (6 CTAs per
+// SM; support tile 128 / 64), 9 the expanded form at 64 x 6. RBF_EVAL_VARIANT selects one for experiments
 // (tools/eval_variants.py).
 template <int MODE, int NT, int TPT, int TILE, int MINB>
 static void launch_eval_variant(const double* targets, int64_t n, const double* sp, const double* sw,
@@ -214,7 +215,7 @@ static void launch_expanded(const double* targets, int64_t n, const double* sp, 
 template <int MODE>
 static void launch_eval(int variant, const double* t, int64_t n, const double* sp, const double* sw, int ns,
                         double inv_r, double* out, cudaStream_t s) {
-  if (ns == 0 && (variant == 0 || variant == 6)) variant = 4;  // expanded form needs an origin support
+  if (ns == 0 && (variant == 0 || variant == 6 || variant == 9)) variant = 4;  // expanded form needs an origin support
   switch (variant) {
     case 0: launch_expanded<MODE, 128, 6, 128, 3>(t, n, sp, sw, ns, inv_r, out, s); break;
     case 6: launch_expanded<MODE, 128, 4, 128, 4>(t, n, sp, sw, ns, inv_r, out, s); break;
@@ -223,6 +224,9 @@ static void launch_eval(int variant, const double* t, int64_t n, const double* s
     case 3: launch_eval_variant<MODE, 64, 8, 128, 4>(t, n, sp, sw, ns, inv_r, out, s); break;
     case 4: launch_eval_variant<MODE, 128, 6, 128, 3>(t, n, sp, sw, ns, inv_r, out, s); break;
     case 5: launch_eval_variant<MODE, 128, 4, 256, 4>(t, n, sp, sw, ns, inv_r, out, s); break;
+    case 7: launch_eval_variant<MODE, 64, 6, 128, 6>(t, n, sp, sw, ns, inv_r, out, s); break;
+    case 8: launch_eval_variant<MODE, 64, 6, 64, 6>(t, n, sp, sw, ns, inv_r, out, s); break;
+    case 9: launch_expanded<MODE, 64, 6, 128, 6>(t, n, sp, sw, ns, inv_r, out, s); break;
     default: launch_eval_variant<MODE, 128, 4, 128, 4>(t, n, sp, sw, ns, inv_r, out, s); break;
   }
 }

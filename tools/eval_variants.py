@@ -26,7 +26,7 @@ for _ in range(10):
 print(best)
 '''
 res = {}
-for v in range(7):
+for v in range(10):
     env = dict(os.environ, RBF_EVAL_VARIANT=str(v))
     r = subprocess.run([sys.executable, "-c", CODE], env=env, capture_output=True, text=True)
     ms = float(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else None
