@@ -196,6 +196,7 @@ typedef struct rbf_gcb_state {
 
 /* rbf_gcb_args.flags */
 #define RBF_GCB_PHASES 1
+#define RBF_GCB_NO_OVERLAP 2 /* MSG path: no next-group scan during appends (A/B tests) */
 
 /* Launch shapes of the selection kernel:
  *  MSG     one 16-CTA cluster, n < 384: the factor rows (owner-stable, row

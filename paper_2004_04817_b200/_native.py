@@ -23,6 +23,7 @@ RBF_EGROW = 5
 RBF_ESTALL = 6
 RBF_EPARSE = 7
 GCB_PHASES = 1  # rbf_gcb_args.flags: record per-phase SM cycles
+GCB_NO_OVERLAP = 2  # rbf_gcb_args.flags: MSG path without the overlapped next-group scan
 STATUS_DONE = 1
 GCB_AUTO = 0
 GCB_CLUSTER = 1

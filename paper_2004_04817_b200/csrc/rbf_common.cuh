@@ -64,17 +64,16 @@ __device__ __forceinline__ double t_from_r2(double r2) {
 }
 
 // Throughput pair: target (px,py,pz) and support (sx,sy,sz) already scaled
-// by 1/R; accumulates w * phi(|p - s|) into (ax, ay, az).
+// by 1/R; pair_phi() returns phi(|p - s|), pair_accum() accumulates
+// w * phi(|p - s|) into (ax, ay, az).
 //
 // FP64-pipe budget per pair: 3 DADD (differences) + 3 (r^2) + 5 (t = 1 - eta)
 // + 4 (q = 5 - 4t = 4 eta + 1, t^2, t^4, t^4 q) + 3 DFMA (accumulate) = 18.
 // t_from_r2() never forms sqrt(r2) separately; see there. r2 below 1e-200 is
 // lifted to 1e-200 (eta = 1e-100 gives phi = 1 exactly, like eta = 0) so the
 // rsqrt never sees zero. The clamp t = max(t, 0) is integer-only.
-__device__ __forceinline__ void pair_accum(double px, double py, double pz,
-                                           double sx, double sy, double sz,
-                                           double wx, double wy, double wz,
-                                           double& ax, double& ay, double& az) {
+__device__ __forceinline__ double pair_phi(double px, double py, double pz,
+                                           double sx, double sy, double sz) {
   const double dx = px - sx, dy = py - sy, dz = pz - sz;
   double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
   const int kTinyHi = 0x16687e92;  // high word of 1e-200
@@ -83,7 +82,14 @@ __device__ __forceinline__ void pair_accum(double px, double py, double pz,
   double t = clamp_nonneg(t_from_r2(r2));
   const double q = fma(-4.0, t, 5.0);
   t = t * t;
-  const double f = (t * t) * q;
+  return (t * t) * q;
+}
+
+__device__ __forceinline__ void pair_accum(double px, double py, double pz,
+                                           double sx, double sy, double sz,
+                                           double wx, double wy, double wz,
+                                           double& ax, double& ay, double& az) {
+  const double f = pair_phi(px, py, pz, sx, sy, sz);
   ax = fma(wx, f, ax);
   ay = fma(wy, f, ay);
   az = fma(wz, f, az);

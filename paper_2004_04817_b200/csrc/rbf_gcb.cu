@@ -323,6 +323,13 @@ struct GlobalPath {
   // memory before the pair loop, so the epilogues never wait on a global
   // load. (An arbitrary S with shared-memory partials filling all 512 lanes
   // measured slower: tools/greedy_ab.py, configs[3].)
+  static constexpr bool kHasOv = false;
+  __device__ bool ov_fits(int, int) { return false; }
+  __device__ int append_ov(int pos, int& n, bool check_dup, double* p2, int, int) {
+    return append(pos, n, check_dup, p2);
+  }
+  __device__ void scan_ov(const int*, const double*, int, int, int) {}
+
   __device__ __forceinline__ void scan(const int* gpos, const double* gpt, const double* gdisp, int card,
                                        int n, int par) {
     const int tid = threadIdx.x, G = gridDim.x;
@@ -835,6 +842,13 @@ struct SmemPath {
     __syncthreads();
   }
 
+  static constexpr bool kHasOv = false;
+  __device__ bool ov_fits(int, int) { return false; }
+  __device__ int append_ov(int pos, int& n, bool check_dup, double* p2, int, int) {
+    return append(pos, n, check_dup, p2);
+  }
+  __device__ void scan_ov(const int*, const double*, int, int, int) {}
+
   __device__ __forceinline__ void scan(const int* gpos, const double* gpt, const double* gdisp, int card, int n,
                        int par) {
     const int tid = threadIdx.x, lane = tid & 31;
@@ -1165,6 +1179,26 @@ constexpr int kMsgOwnElems = 8 * kMsgOwnRows * (kMsgOwnRows - 1) + kMsgOwnRows *
 // column-owned copy of Li: column j = 16 q + rank holds rows j .. kMsgMax-1
 constexpr int kMsgColElems = kMsgOwnRows * kMsgMax - 8 * kMsgOwnRows * (kMsgOwnRows - 1);
 constexpr int kMsgGoff = 512;   // group offsets cached in shared memory (else read from L2)
+// Overlapped group scans (MsgPath::ov_scan_a / scan_ov): while warps
+// 0..kAppWarps-1 append a support, the other kOvWarps warps (one per TMEM
+// lane quadrant) evaluate the next group's kernel values phi(|p - s_j|) for
+// every support including the one being appended and keep them in tensor
+// memory; after the append the group scan is sum_j x'_j phi_j from TMEM
+// (3 FMAs per pair instead of 18 FP64 instructions), shared by all warps.
+constexpr int kAppWarps = 12;
+constexpr int kOvWarps = kLoopWarps - kAppWarps;
+static_assert(kOvWarps == 4, "one overlap-scan warp per TMEM lane quadrant");
+constexpr int kOvRowsMax = 128;  // rows of a group per CTA
+constexpr int kTmemCols = 512;   // 32-bit columns per TMEM lane (all of it)
+#ifndef RBF_OV_R
+#define RBF_OV_R 4
+#endif
+constexpr int kOvR = RBF_OV_R;   // rows per overlap row group
+constexpr int kOvC = 16 / kOvR;  // support columns per step: 16 pair chains per lane
+#ifndef RBF_OV_SLEEP_NS
+#define RBF_OV_SLEEP_NS 0
+#endif
+constexpr unsigned kOvSleepNs = RBF_OV_SLEEP_NS;
 
 enum MsgBar { kMbScan0 = 0, kMbScan1, kMbC0, kMbR, kMbC1, kMbW, kMbCount };
 
@@ -1182,6 +1216,14 @@ struct MsgShared {
   double part_in[2][kClusterCTAs][2][2];           // scan partials (err, pos as double)
   double acc[kLoopWarps][4][4];
   int goff[kMsgGoff + 1];
+  double ov_p[kOvRowsMax][3];        // overlap scan: this CTA's rows of the next group: scaled points,
+  double ov_d[kOvRowsMax][3];        // displacements,
+  int ov_pos[kOvRowsMax];            // positions
+  unsigned char ov_el[kOvRowsMax];   // and eligibility (read after the append marked its node)
+  unsigned tmem_base;        // TMEM allocation (kTmemCols columns)
+  int ov_res, ov_n;          // append result / n after it, for the scan warps
+  int ov_group, ov_nold;     // overlap valid for group ov_group, computed at n = ov_nold
+  unsigned ov_bits;          // mbarrier phase bits of the append warps
   alignas(8) unsigned long long mbar[kMbCount];
 };
 static_assert(sizeof(MsgShared) <= 227 * 1024, "MsgShared exceeds shared memory");
@@ -1498,15 +1540,294 @@ struct MsgPath {
     pc.mark(14);
   }
 
+  // ------------------------------------------------------------- overlap
+  static constexpr bool kHasOv = true;
+  __device__ __forceinline__ void bar_ov() { asm volatile("bar.sync 2, %0;" ::"n"(kLoopThreads) : "memory"); }
+  template <bool kOv>
+  __device__ __forceinline__ void sync_a() {
+    if (kOv)
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kAppWarps) : "memory");
+    else
+      __syncthreads();
+  }
+  __device__ __forceinline__ static void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
+  __device__ __forceinline__ static void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
+  // all of TMEM for this CTA (one CTA per SM), allocated by the last warp
+  __device__ void tmem_alloc() {
+    if ((threadIdx.x >> 5) == kLoopWarps - 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&sh.tmem_base)),
+                   "n"(kTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
+  __device__ void tmem_free() {
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if ((threadIdx.x >> 5) == kLoopWarps - 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sh.tmem_base), "n"(kTmemCols)
+                   : "memory");
+  }
+  // 4 doubles of this thread <-> 8 consecutive 32-bit columns of its TMEM lane
+  __device__ __forceinline__ static void tmem_st4(unsigned taddr, const double (&f)[4]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+        "r"(__double2loint(f[0])), "r"(__double2hiint(f[0])), "r"(__double2loint(f[1])), "r"(__double2hiint(f[1])),
+        "r"(__double2loint(f[2])), "r"(__double2hiint(f[2])), "r"(__double2loint(f[3])), "r"(__double2hiint(f[3]))
+        : "memory");
+  }
+  __device__ __forceinline__ static void tmem_st8(unsigned taddr, const double (&f)[8]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16};" ::"r"(taddr),
+        "r"(__double2loint(f[0])), "r"(__double2hiint(f[0])), "r"(__double2loint(f[1])), "r"(__double2hiint(f[1])),
+        "r"(__double2loint(f[2])), "r"(__double2hiint(f[2])), "r"(__double2loint(f[3])), "r"(__double2hiint(f[3])),
+        "r"(__double2loint(f[4])), "r"(__double2hiint(f[4])), "r"(__double2loint(f[5])), "r"(__double2hiint(f[5])),
+        "r"(__double2loint(f[6])), "r"(__double2hiint(f[6])), "r"(__double2loint(f[7])), "r"(__double2hiint(f[7]))
+        : "memory");
+  }
+  __device__ __forceinline__ static void tmem_st16(unsigned taddr, const double (&f)[16]) {
+    unsigned r[32];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      r[2 * i] = (unsigned)__double2loint(f[i]);
+      r[2 * i + 1] = (unsigned)__double2hiint(f[i]);
+    }
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+  }
+  __device__ __forceinline__ static void tmem_ld4(unsigned taddr, double (&f)[4]) {
+    unsigned r0, r1, r2, r3, r4, r5, r6, r7;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3), "=r"(r4), "=r"(r5), "=r"(r6), "=r"(r7)
+                 : "r"(taddr)
+                 : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    f[0] = __hiloint2double((int)r1, (int)r0);
+    f[1] = __hiloint2double((int)r3, (int)r2);
+    f[2] = __hiloint2double((int)r5, (int)r4);
+    f[3] = __hiloint2double((int)r7, (int)r6);
+  }
+
+  // 16 doubles (4 column chunks of 4) in one load, one wait
+  __device__ __forceinline__ static void tmem_ld16(unsigned taddr, double (&f)[16]) {
+    unsigned r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr)
+        : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) f[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
+  }
+
+  // can the next group (card rows) be scanned during an append at n supports
+  __device__ bool ov_fits(int card, int n) {
+    if ((a.flags & RBF_GCB_NO_OVERLAP) || nclusters() != 1 || n + 1 >= kMsgMax) return false;
+    const int rows = (card + kClusterCTAs - 1) / kClusterCTAs;
+    if (rows > kOvRowsMax) return false;
+    const int rounds = ((rows + kOvR - 1) / kOvR + kOvWarps - 1) / kOvWarps;
+    const int ji = (n + 1 + 31) >> 5;
+    return 2 * kOvR * rounds * ov_stride(ji) <= kTmemCols;
+  }
+
+  // TMEM layout of the overlap: scan warp qd (lane quadrant qd) keeps the
+  // row groups rg = qd, qd + 4, ... (round r = rg >> 2) of kOvR rows; its
+  // lane holds, per round, chunks ji = 0 .. ji_n-1 (columns j = 32 ji +
+  // lane) of kOvR doubles at 32-bit column 2 kOvR (r * stride + ji).
+  __device__ __forceinline__ static int ov_stride(int ji_n) { return (ji_n + kOvC - 1) / kOvC * kOvC; }
+
+  // Scan warps, during the append of support n (coordinates s*, scaled):
+  // phi of the next group's rows against supports 0 .. n (n: the new one),
+  // kOvC columns at a time (kOvR * kOvC independent pair chains per lane:
+  // one warp per SMSP keeps the FP64 pipe busy on its own), into TMEM; the
+  // rows' positions and displacements into shared memory.
+  __device__ void ov_scan_a(int off, int card, int n, double spx, double spy, double spz) {
+    static_assert(kOvR * kOvC == 16, "one 32x32b.x32 TMEM store per step");
+    const int wq = (threadIdx.x >> 5) - kAppWarps, lane = threadIdx.x & 31;
+    const unsigned b = blockIdx.x;
+    const int lo = (int)(((unsigned)card * b) >> 4), hi = (int)(((unsigned)card * (b + 1)) >> 4);
+    const int ng = (hi - lo + kOvR - 1) / kOvR, ji_n = (n + 1 + 31) >> 5, stride = ov_stride(ji_n);
+    const unsigned tl = sh.tmem_base + ((unsigned)(32 * wq) << 16);
+    const double* gpt = s.gpt + 3 * (int64_t)off;
+    // this warp's rows (groups rg = wq + 4 r) -> shared memory in one round trip
+    for (int k = lane; k < kOvRowsMax; k += 32) {
+      const int i = kOvR * (wq + kOvWarps * (k / kOvR)) + k % kOvR, t = lo + i;
+      if (t >= hi) break;
+      sh.ov_pos[i] = __ldg(a.group_pos + off + t);
+      sh.ov_p[i][0] = __ldcg(gpt + 3 * (int64_t)t) * inv_r;
+      sh.ov_p[i][1] = __ldcg(gpt + 3 * (int64_t)t + 1) * inv_r;
+      sh.ov_p[i][2] = __ldcg(gpt + 3 * (int64_t)t + 2) * inv_r;
+      sh.ov_d[i][0] = __ldcg(s.gdisp + 3 * ((int64_t)off + t));
+      sh.ov_d[i][1] = __ldcg(s.gdisp + 3 * ((int64_t)off + t) + 1);
+      sh.ov_d[i][2] = __ldcg(s.gdisp + 3 * ((int64_t)off + t) + 2);
+    }
+    __syncwarp();
+    int r = 0;
+    for (int rg = wq; rg < ng; rg += kOvWarps, ++r) {
+      double px[kOvR], py[kOvR], pz[kOvR];
+#pragma unroll
+      for (int q = 0; q < kOvR; ++q) {
+        const int i = kOvR * rg + q;
+        const bool ok = lo + i < hi;
+        px[q] = ok ? sh.ov_p[i][0] : 0.0;
+        py[q] = ok ? sh.ov_p[i][1] : 0.0;
+        pz[q] = ok ? sh.ov_p[i][2] : 0.0;
+      }
+#pragma unroll 1
+      for (int ji = 0; ji < ji_n; ji += kOvC) {
+        double f[16];
+#pragma unroll
+        for (int h = 0; h < kOvC; ++h) {
+          const int j = 32 * (ji + h) + lane;
+          const bool old = j < n, add = j == n;
+          const int jj = old ? j : 0;
+          const double sx = add ? spx : sh.sx[jj], sy = add ? spy : sh.sy[jj], sz = add ? spz : sh.sz[jj];
+#pragma unroll
+          for (int q = 0; q < kOvR; ++q) {
+            const double fq = pair_phi(px[q], py[q], pz[q], sx, sy, sz);
+            f[kOvR * h + q] = (old || add) ? fq : 0.0;
+          }
+        }
+        tmem_st16(tl + 2u * kOvR * (unsigned)(r * stride + ji), f);
+      }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  // scan warps after bar_ov (the append has marked its node ineligible)
+  __device__ void ov_eligibility(int card) {
+    const int wq = (threadIdx.x >> 5) - kAppWarps, lane = threadIdx.x & 31;
+    const unsigned b = blockIdx.x;
+    const int lo = (int)(((unsigned)card * b) >> 4), hi = (int)(((unsigned)card * (b + 1)) >> 4);
+    for (int i = 32 * wq + lane; i < hi - lo; i += 32 * kOvWarps)
+      sh.ov_el[i] = !__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + sh.ov_pos[i]);
+  }
+
+  // The scan of the group whose kernel values ov_scan_a stored, after the
+  // append (n supports now, weights x'): every warp takes rounds of its lane
+  // quadrant (warps w, w + 4, w + 8, w + 12 share quadrant w % 4), sums
+  // x'_j phi_j over its lanes' columns in increasing j, butterfly-sums the
+  // lanes and finishes errors, arg-max partials and publication as scan().
+  __device__ void scan_ov(const int*, const double*, int card, int n, int par) {
+    Best bu{-1.0, kNone}, br{-1.0, kNone};
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qd = warp & 3, wr = warp >> 2;
+    const unsigned b = blockIdx.x;
+    const int lo = (int)(((unsigned)card * b) >> 4), hi = (int)(((unsigned)card * (b + 1)) >> 4);
+    const int ng = (hi - lo + kOvR - 1) / kOvR, ji_n = (n + 31) >> 5, stride = ov_stride(ji_n);
+    const unsigned tl = sh.tmem_base + ((unsigned)(32 * qd) << 16);
+    // rounds of quadrant qd: rg = qd + 4 r < ng; this warp: r = wr, wr + 4, ..
+    for (int r = wr; qd + 4 * r < ng; r += 4) {
+      const int rg = qd + 4 * r;
+      double v[3 * kOvR];
+#pragma unroll
+      for (int e = 0; e < 3 * kOvR; ++e) v[e] = 0.0;
+#pragma unroll 1
+      for (int j0 = 0; j0 < ji_n; j0 += kOvC) {
+        double f[16];
+        tmem_ld16(tl + 2u * kOvR * (unsigned)(r * stride + j0), f);
+#pragma unroll
+        for (int h = 0; h < kOvC; ++h) {
+          const int j = 32 * (j0 + h) + lane;
+          const bool in = j < n;
+          const int jj = in ? j : 0;
+          const double wx = in ? sh.wx[jj] : 0.0, wy = in ? sh.wy[jj] : 0.0, wz = in ? sh.wz[jj] : 0.0;
+#pragma unroll
+          for (int q = 0; q < kOvR; ++q) {
+            v[3 * q] = fma(wx, f[kOvR * h + q], v[3 * q]);
+            v[3 * q + 1] = fma(wy, f[kOvR * h + q], v[3 * q + 1]);
+            v[3 * q + 2] = fma(wz, f[kOvR * h + q], v[3 * q + 2]);
+          }
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 3 * kOvR; ++e)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[e] += __shfl_xor_sync(0xffffffffu, v[e], o);
+      const int i = kOvR * rg + lane, t = lo + i;
+      if (lane < kOvR && t < hi) {
+        double ux = v[0], uy = v[1], uz = v[2];
+#pragma unroll
+        for (int q = 1; q < kOvR; ++q)
+          if (lane == q) {
+            ux = v[3 * q];
+            uy = v[3 * q + 1];
+            uz = v[3 * q + 2];
+          }
+        const double e = residual_norm(sh.ov_d[i][0], sh.ov_d[i][1], sh.ov_d[i][2], ux, uy, uz);
+        s.err[t] = e;
+        const int pos = sh.ov_pos[i];
+        if (better(e, pos, bu.err, bu.pos)) bu = Best{e, pos};
+        if (sh.ov_el[i] && better(e, pos, br.err, br.pos)) br = Best{e, pos};
+      }
+    }
+    pc.mark(11);
+    cta_best2(sh.cm, bu, br, kOvR);
+    if (threadIdx.x < 32) publish2(bu, br, par);
+    pc.mark(14);
+  }
+
+  // append of `pos` with the scan of the next group (off, card) overlapped
+  __device__ int append_ov(int pos, int& n, bool check_dup, double* pivot2_out, int off, int card) {
+    const int n0 = n;
+    int res = kAccepted;
+    double p2 = 0.0;
+    if ((threadIdx.x >> 5) < kAppWarps) {
+      res = append_t<true>(pos, n, check_dup, &p2);
+    } else {
+      ov_scan_a(off, card, n0, __ldg(a.points + 3 * (int64_t)pos) * inv_r,
+                __ldg(a.points + 3 * (int64_t)pos + 1) * inv_r, __ldg(a.points + 3 * (int64_t)pos + 2) * inv_r);
+      bar_ov();
+      ov_eligibility(card);
+    }
+    if (threadIdx.x == 0) {
+      sh.ov_res = res;
+      sh.ov_n = n;
+      sh.ov_bits = phase_bits;
+      sh.cm.dbl[5] = p2;
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    res = sh.ov_res;
+    n = sh.ov_n;
+    phase_bits = sh.ov_bits;  // the scan warps skipped the append's waits
+    *pivot2_out = sh.cm.dbl[5];
+    return res;
+  }
+  __device__ int append(int pos, int& n, bool check_dup, double* pivot2_out) {
+    return append_t<false>(pos, n, check_dup, pivot2_out);
+  }
+
   // ------------------------------------------------------------------ append
   // owned rows: q = 0.. with i = 16 q + rank < n (q < 24 here); warp w takes
   // q = w and q = w + 16 together, so no warp handles two rows one after the
   // other
-  template <typename F>
+  template <int kW, typename F>
   __device__ __forceinline__ void for_owned_row_pairs(int n, F&& body) {
     const int warp = threadIdx.x >> 5, rk = rank();
-    for (int q = warp; 16 * q + rk < n; q += 2 * kLoopWarps) {
-      const int qb = q + kLoopWarps;
+    for (int q = warp; 16 * q + rk < n; q += 2 * kW) {
+      const int qb = q + kW;
       body(q, 16 * q + rk, 16 * qb + rk < n ? qb : -1, 16 * qb + rk);
     }
   }
@@ -1554,23 +1875,39 @@ struct MsgPath {
     if (lane < kClusterCTAs) st_async(raddr(&vec[i], lane), v, rbar(bar, lane));
   }
 
-  __device__ int append(int pos, int& n, bool check_dup, double* pivot2_out) {
+  // kOv: warps 0..kAppWarps-1 only (the others scan the next group
+  // meanwhile, ov_scan_a); every path of the append passes bar_ov() exactly
+  // once, before the weights are updated
+  template <bool kOv>
+  __device__ int append_t(int pos, int& n, bool check_dup, double* pivot2_out) {
+    constexpr int kWA = kOv ? kAppWarps : kLoopWarps, kTA = 32 * kWA;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rk = rank();
     const int cap = a.cap;
     const double px = __ldg(a.points + 3 * (int64_t)pos), py = __ldg(a.points + 3 * (int64_t)pos + 1),
                  pz = __ldg(a.points + 3 * (int64_t)pos + 2);
-    const bool near = exact_row(sh.cm, sh.row, n, px, py, pz, a.radius, a.dup_dist,
-                                  [&](int j, double& x, double& y, double& z) {
-                                    x = sh.ux[j];
-                                    y = sh.uy[j];
-                                    z = sh.uz[j];
-                                  });
-    if (check_dup && n > 0 && near) return kRejectDup;
+    bool near;
+    {  // exact_row() over the append warps
+      if (tid == 0) sh.cm.dbl[0] = 0.0;
+      sync_a<kOv>();
+      bool nr = false;
+      for (int j = tid; j < n; j += kTA) {
+        const double d = cdist_exact(px, py, pz, sh.ux[j], sh.uy[j], sh.uz[j]);
+        sh.row[j] = phi_exact(d, a.radius);
+        nr |= d < a.dup_dist;
+      }
+      if (__any_sync(0xffffffffu, nr) && lane == 0) sh.cm.dbl[0] = 1.0;
+      sync_a<kOv>();
+      near = sh.cm.dbl[0] != 0.0;
+    }
+    if (check_dup && n > 0 && near) {
+      if (kOv) bar_ov();
+      return kRejectDup;
+    }
     pc.mark(1);
     // c0 = Li row
     expect(kMbC0, n * 8);
-    for_owned_row_pairs(n, [&](int qa, int ia, int qb, int ib) {
+    for_owned_row_pairs<kWA>(n, [&](int qa, int ia, int qb, int ib) {
       double va, vb;
       own_dot2(sh.Liown, qa, ia, qb, ib, [&](int j) { return sh.row[j]; }, lane, va, vb);
       bcast(sh.c0, ia, va, kMbC0, lane);
@@ -1580,7 +1917,7 @@ struct MsgPath {
     pc.mark(2);
     // r = row - L c0
     expect(kMbR, n * 8);
-    for_owned_row_pairs(n, [&](int qa, int ia, int qb, int ib) {
+    for_owned_row_pairs<kWA>(n, [&](int qa, int ia, int qb, int ib) {
       double va, vb;
       own_dot2(sh.Lown, qa, ia, qb, ib, [&](int j) { return sh.c0[j]; }, lane, va, vb);
       bcast(sh.r, ia, sh.row[ia] - va, kMbR, lane);
@@ -1591,7 +1928,7 @@ struct MsgPath {
     // c = c0 + Li r, partial sums of c.c and c.y over the owned rows
     expect(kMbC1, n * 8 + kClusterCTAs * 32);
     double pcc = 0.0, pcy0 = 0.0, pcy1 = 0.0, pcy2 = 0.0;
-    for_owned_row_pairs(n, [&](int qa, int ia, int qb, int ib) {
+    for_owned_row_pairs<kWA>(n, [&](int qa, int ia, int qb, int ib) {
       double va, vb;
       own_dot2(sh.Liown, qa, ia, qb, ib, [&](int j) { return sh.r[j]; }, lane, va, vb);
       const double ca = sh.c0[ia] + va;
@@ -1616,11 +1953,11 @@ struct MsgPath {
       cm.wred[warp][2] = pcy1;
       cm.wred[warp][3] = pcy2;
     }
-    __syncthreads();
+    sync_a<kOv>();
     if (tid < 4 * kClusterCTAs) {  // CTA partial (warp order) -> every CTA
       const int c = tid & 3, dst = tid >> 2;
       double t = 0.0;
-      for (int w = 0; w < kLoopWarps; ++w) t += cm.wred[w][c];
+      for (int w = 0; w < kWA; ++w) t += cm.wred[w][c];
       st_async(raddr(&sh.rpart[rk][c], dst), t, rbar(kMbC1, dst));
     }
     wait(kMbC1);
@@ -1630,11 +1967,12 @@ struct MsgPath {
       for (int c = 0; c < kClusterCTAs; ++c) t += sh.rpart[c][tid];
       cm.dbl[1 + tid] = t;
     }
-    __syncthreads();
+    sync_a<kOv>();
     const double pivot2 = 1.0 - cm.dbl[1];  // row[n] = phi(0) = 1 exactly
     *pivot2_out = pivot2;
     if (!(pivot2 > 0.0)) {
-      __syncthreads();
+      sync_a<kOv>();
+      if (kOv) bar_ov();
       return kRejectPivot;
     }
     const double l = sqrt(pivot2);
@@ -1650,8 +1988,8 @@ struct MsgPath {
     const double neg_inv_l = -inv_l;
     expect(kMbW, (unsigned)(n * 8));
     // warp w takes owned columns qc = w and w + 16 together
-    for (int qa = warp; 16 * qa + rk < n; qa += 2 * kLoopWarps) {
-      const int qb = qa + kLoopWarps;
+    for (int qa = warp; 16 * qa + rk < n; qa += 2 * kWA) {
+      const int qb = qa + kWA;
       const int ja = 16 * qa + rk, jb = 16 * qb + rk;
       const bool has_b = jb < n;
       const double* ca = sh.Licol + own_col_off(qa, rk);
@@ -1722,7 +2060,7 @@ struct MsgPath {
     if (rk == owner) {  // row n of L = [c, l] (c replicated), diagonal of Li
       const int o = own_off(qn, owner);
       const bool global_copy = cluster() == 0;
-      for (int j = tid; j < n; j += kLoopThreads) {
+      for (int j = tid; j < n; j += kTA) {
         sh.Lown[o + j] = sh.c1[j];
         if (global_copy) a.L[tri_off(n) + j] = sh.c1[j];
       }
@@ -1732,7 +2070,8 @@ struct MsgPath {
       }
     }
     wait(kMbW);
-    for (int j = tid; j < n; j += kLoopThreads) {  // x' = x + Li[n][j] y_n
+    if (kOv) bar_ov();  // the next group's scan has read the old weights
+    for (int j = tid; j < n; j += kTA) {  // x' = x + Li[n][j] y_n
       const double lij = sh.u_all[j] * neg_inv_l;
       sh.wx[j] = fma(lij, yn0, sh.wx[j]);
       sh.wy[j] = fma(lij, yn1, sh.wy[j]);
@@ -1751,7 +2090,7 @@ struct MsgPath {
       sh.wz[n] = yn2 * inv_l;
     }
     n += 1;
-    __syncthreads();
+    sync_a<kOv>();
     pc.mark(5);
     return kAccepted;
   }
@@ -1893,6 +2232,7 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
 
   const int card_max = (a.nb + m - 1) / m;
   int gk = k % m;
+  int ov_group = -1;  // group whose scan ran during the last append (MsgPath)
   while (!done_loop) {
     if (n >= a.max_supports) {
       done_loop = 1;
@@ -1923,7 +2263,11 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
     const int card = P.group_off(gi + 1) - off;
     const int* gpos = a.group_pos + off;
     pc.mark(6);
-    P.scan(gpos, s.gpt + 3 * (int64_t)off, s.gdisp + 3 * (int64_t)off, card, n, par);
+    if (ov_group == gi)  // rows evaluated during the last append
+      P.scan_ov(gpos, s.gdisp + 3 * (int64_t)off, card, n, par);
+    else
+      P.scan(gpos, s.gpt + 3 * (int64_t)off, s.gdisp + 3 * (int64_t)off, card, n, par);
+    ov_group = -1;
     P.gather(par, 2);
     pc.mark(0);
     pc.count(10);
@@ -1936,13 +2280,23 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
     bool added = false;
     int added_pos = -1;
     if (local_max > a.tol) {
+      // the next group's scan runs during the append when it fits
+      const int gn = gk + 1 == m ? 0 : gk + 1;
+      int ov_g = -1, ov_off = 0, ov_card = 0;
+      if (Path::kHasOv) {
+        ov_off = P.group_off(gn);
+        ov_card = P.group_off(gn + 1) - ov_off;
+        if (P.ov_fits(ov_card, n)) ov_g = gn;
+      }
       while (cand.pos != kNone && cand.err > a.tol) {
         double p2;
-        const int res = P.append(cand.pos, n, true, &p2);
+        const int res = ov_g >= 0 ? P.append_ov(cand.pos, n, true, &p2, ov_off, ov_card)
+                                  : P.append(cand.pos, n, true, &p2);
         pc.count(9);
         if (res == kAccepted) {
           added = true;
           added_pos = cand.pos;
+          ov_group = ov_g;
           break;
         }
         if (tid == 0) {
@@ -2054,8 +2408,10 @@ __global__ void __launch_bounds__(kLoopThreads, 1) gcb_msg_kernel(rbf_gcb_args a
   PhaseClockT<kPh> pc;
   pc.start(sh.cm.phase);
   MsgPath<PhaseClockT<kPh>> P{a, s, sh, 1.0 / a.radius, pc, 0u, 0u};
+  P.tmem_alloc();
   gcb_driver(P, a, s, pc, RBF_GCB_MSG);
   P.finish();
+  P.tmem_free();
 }
 
 static int resolve_mode(int mode, int nb, int m) {

@@ -543,6 +543,8 @@ def _gcb_run(boundary, config, mode=None, phases=None):
     if phases is None:  # RBF_GCB_PHASES=1: per-phase device cycles in history.device_phase_cycles
         phases = os.environ.get("RBF_GCB_PHASES", "") == "1"
     args.flags = N.GCB_PHASES if phases else 0
+    if os.environ.get("RBF_GCB_OVERLAP", "1") == "0":  # A/B: no next-group scan during appends
+        args.flags |= N.GCB_NO_OVERLAP
     args.radius = radius
     args.tol = float(config.tol)
     args.dup_dist = NEAR_DUPLICATE_FRACTION * config.radius
