@@ -1193,8 +1193,13 @@ constexpr int kTmemCols = 512;   // 32-bit columns per TMEM lane (all of it)
 #ifndef RBF_OV_R
 #define RBF_OV_R 4
 #endif
+#ifndef RBF_OV_C
+#define RBF_OV_C (8 / RBF_OV_R)
+#endif
 constexpr int kOvR = RBF_OV_R;   // rows per overlap row group
-constexpr int kOvC = 16 / kOvR;  // support columns per step: 16 pair chains per lane
+constexpr int kOvC = RBF_OV_C;   // support columns per ov_scan_a step: kOvR * kOvC pair chains per lane
+constexpr int kOvLd = 16 / kOvR; // chunks per scan_ov TMEM load (16 doubles)
+static_assert(kOvR * kOvC == 16 || kOvR * kOvC == 8, "one TMEM store per step");
 #ifndef RBF_OV_SLEEP_NS
 #define RBF_OV_SLEEP_NS 0
 #endif
@@ -1585,7 +1590,7 @@ struct MsgPath {
         "r"(__double2loint(f[2])), "r"(__double2hiint(f[2])), "r"(__double2loint(f[3])), "r"(__double2hiint(f[3]))
         : "memory");
   }
-  __device__ __forceinline__ static void tmem_st8(unsigned taddr, const double (&f)[8]) {
+  __device__ __forceinline__ static void tmem_st8(unsigned taddr, const double* f) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
         "%14, %15, %16};" ::"r"(taddr),
@@ -1595,7 +1600,7 @@ struct MsgPath {
         "r"(__double2loint(f[6])), "r"(__double2hiint(f[6])), "r"(__double2loint(f[7])), "r"(__double2hiint(f[7]))
         : "memory");
   }
-  __device__ __forceinline__ static void tmem_st16(unsigned taddr, const double (&f)[16]) {
+  __device__ __forceinline__ static void tmem_st16(unsigned taddr, const double* f) {
     unsigned r[32];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -1655,7 +1660,10 @@ struct MsgPath {
   // row groups rg = qd, qd + 4, ... (round r = rg >> 2) of kOvR rows; its
   // lane holds, per round, chunks ji = 0 .. ji_n-1 (columns j = 32 ji +
   // lane) of kOvR doubles at 32-bit column 2 kOvR (r * stride + ji).
-  __device__ __forceinline__ static int ov_stride(int ji_n) { return (ji_n + kOvC - 1) / kOvC * kOvC; }
+  __device__ __forceinline__ static int ov_stride(int ji_n) {
+    constexpr int kQ = kOvC > kOvLd ? kOvC : kOvLd;
+    return (ji_n + kQ - 1) / kQ * kQ;
+  }
 
   // Scan warps, during the append of support n (coordinates s*, scaled):
   // phi of the next group's rows against supports 0 .. n (n: the new one),
@@ -1663,7 +1671,6 @@ struct MsgPath {
   // one warp per SMSP keeps the FP64 pipe busy on its own), into TMEM; the
   // rows' positions and displacements into shared memory.
   __device__ void ov_scan_a(int off, int card, int n, double spx, double spy, double spz) {
-    static_assert(kOvR * kOvC == 16, "one 32x32b.x32 TMEM store per step");
     const int wq = (threadIdx.x >> 5) - kAppWarps, lane = threadIdx.x & 31;
     const unsigned b = blockIdx.x;
     const int lo = (int)(((unsigned)card * b) >> 4), hi = (int)(((unsigned)card * (b + 1)) >> 4);
@@ -1696,7 +1703,7 @@ struct MsgPath {
       }
 #pragma unroll 1
       for (int ji = 0; ji < ji_n; ji += kOvC) {
-        double f[16];
+        double f[kOvR * kOvC];
 #pragma unroll
         for (int h = 0; h < kOvC; ++h) {
           const int j = 32 * (ji + h) + lane;
@@ -1709,7 +1716,10 @@ struct MsgPath {
             f[kOvR * h + q] = (old || add) ? fq : 0.0;
           }
         }
-        tmem_st16(tl + 2u * kOvR * (unsigned)(r * stride + ji), f);
+        if constexpr (kOvR * kOvC == 16)
+          tmem_st16(tl + 2u * kOvR * (unsigned)(r * stride + ji), f);
+        else
+          tmem_st8(tl + 2u * kOvR * (unsigned)(r * stride + ji), f);
       }
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -1739,47 +1749,44 @@ struct MsgPath {
     // rounds of quadrant qd: rg = qd + 4 r < ng; this warp: r = wr, wr + 4, ..
     for (int r = wr; qd + 4 * r < ng; r += 4) {
       const int rg = qd + 4 * r;
-      double v[3 * kOvR];
+      static_assert(kOvR == 4, "scan_ov reduce-scatters 4 rows x 4 slots");
+      double v[16];
 #pragma unroll
-      for (int e = 0; e < 3 * kOvR; ++e) v[e] = 0.0;
+      for (int e = 0; e < 16; ++e) v[e] = 0.0;
 #pragma unroll 1
-      for (int j0 = 0; j0 < ji_n; j0 += kOvC) {
+      for (int j0 = 0; j0 < ji_n; j0 += kOvLd) {
         double f[16];
         tmem_ld16(tl + 2u * kOvR * (unsigned)(r * stride + j0), f);
 #pragma unroll
-        for (int h = 0; h < kOvC; ++h) {
+        for (int h = 0; h < kOvLd; ++h) {
           const int j = 32 * (j0 + h) + lane;
           const bool in = j < n;
           const int jj = in ? j : 0;
           const double wx = in ? sh.wx[jj] : 0.0, wy = in ? sh.wy[jj] : 0.0, wz = in ? sh.wz[jj] : 0.0;
 #pragma unroll
-          for (int q = 0; q < kOvR; ++q) {
-            v[3 * q] = fma(wx, f[kOvR * h + q], v[3 * q]);
-            v[3 * q + 1] = fma(wy, f[kOvR * h + q], v[3 * q + 1]);
-            v[3 * q + 2] = fma(wz, f[kOvR * h + q], v[3 * q + 2]);
+          for (int q = 0; q < 4; ++q) {
+            v[4 * q] = fma(wx, f[4 * h + q], v[4 * q]);
+            v[4 * q + 1] = fma(wy, f[4 * h + q], v[4 * q + 1]);
+            v[4 * q + 2] = fma(wz, f[4 * h + q], v[4 * q + 2]);
           }
         }
       }
-#pragma unroll
-      for (int e = 0; e < 3 * kOvR; ++e)
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v[e] += __shfl_xor_sync(0xffffffffu, v[e], o);
-      const int i = kOvR * rg + lane, t = lo + i;
-      if (lane < kOvR && t < hi) {
-        double ux = v[0], uy = v[1], uz = v[2];
-#pragma unroll
-        for (int q = 1; q < kOvR; ++q)
-          if (lane == q) {
-            ux = v[3 * q];
-            uy = v[3 * q + 1];
-            uz = v[3 * q + 2];
-          }
-        const double e = residual_norm(sh.ov_d[i][0], sh.ov_d[i][1], sh.ov_d[i][2], ux, uy, uz);
+      if (r == 0) pc.mark(12);
+      int idx;
+      const double tot = warp_reduce_scatter16(v, lane, idx);
+      if ((lane & 1) == 0 && (idx & 3) != 3) sh.acc[warp][idx >> 2][idx & 3] = tot;
+      __syncwarp();
+      if (r == 0) pc.mark(13);
+      const int i = 4 * rg + lane, t = lo + i;
+      if (lane < 4 && t < hi) {
+        const double e = residual_norm(sh.ov_d[i][0], sh.ov_d[i][1], sh.ov_d[i][2], sh.acc[warp][lane][0],
+                                       sh.acc[warp][lane][1], sh.acc[warp][lane][2]);
         s.err[t] = e;
         const int pos = sh.ov_pos[i];
         if (better(e, pos, bu.err, bu.pos)) bu = Best{e, pos};
         if (sh.ov_el[i] && better(e, pos, br.err, br.pos)) br = Best{e, pos};
       }
+      __syncwarp();
     }
     pc.mark(11);
     cta_best2(sh.cm, bu, br, kOvR);
