@@ -1224,7 +1224,8 @@ struct MsgShared {
   double ov_p[kOvRowsMax][3];        // overlap scan: this CTA's rows of the next group: scaled points,
   double ov_d[kOvRowsMax][3];        // displacements,
   int ov_pos[kOvRowsMax];            // positions
-  unsigned char ov_el[kOvRowsMax];   // and eligibility (read after the append marked its node)
+  unsigned char ov_el[kOvRowsMax];   // and eligibility (but for the node being appended, ov_added)
+  int ov_added;                      // node appended while the rows were evaluated
   unsigned tmem_base;        // TMEM allocation (kTmemCols columns)
   int ov_res, ov_n;          // append result / n after it, for the scan warps
   int ov_group, ov_nold;     // overlap valid for group ov_group, computed at n = ov_nold
@@ -1681,7 +1682,11 @@ struct MsgPath {
     for (int k = lane; k < kOvRowsMax; k += 32) {
       const int i = kOvR * (wq + kOvWarps * (k / kOvR)) + k % kOvR, t = lo + i;
       if (t >= hi) break;
-      sh.ov_pos[i] = __ldg(a.group_pos + off + t);
+      const int pos = __ldg(a.group_pos + off + t);
+      sh.ov_pos[i] = pos;
+      // eligibility: only the node being appended can change before scan_ov
+      // (rejected candidates are marked before the next attempt re-runs this)
+      sh.ov_el[i] = !__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + pos);
       sh.ov_p[i][0] = __ldcg(gpt + 3 * (int64_t)t) * inv_r;
       sh.ov_p[i][1] = __ldcg(gpt + 3 * (int64_t)t + 1) * inv_r;
       sh.ov_p[i][2] = __ldcg(gpt + 3 * (int64_t)t + 2) * inv_r;
@@ -1724,15 +1729,6 @@ struct MsgPath {
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
-  // scan warps after bar_ov (the append has marked its node ineligible)
-  __device__ void ov_eligibility(int card) {
-    const int wq = (threadIdx.x >> 5) - kAppWarps, lane = threadIdx.x & 31;
-    const unsigned b = blockIdx.x;
-    const int lo = (int)(((unsigned)card * b) >> 4), hi = (int)(((unsigned)card * (b + 1)) >> 4);
-    for (int i = 32 * wq + lane; i < hi - lo; i += 32 * kOvWarps)
-      sh.ov_el[i] = !__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + sh.ov_pos[i]);
-  }
-
   // The scan of the group whose kernel values ov_scan_a stored, after the
   // append (n supports now, weights x'): every warp takes rounds of its lane
   // quadrant (warps w, w + 4, w + 8, w + 12 share quadrant w % 4), sums
@@ -1784,7 +1780,7 @@ struct MsgPath {
         s.err[t] = e;
         const int pos = sh.ov_pos[i];
         if (better(e, pos, bu.err, bu.pos)) bu = Best{e, pos};
-        if (sh.ov_el[i] && better(e, pos, br.err, br.pos)) br = Best{e, pos};
+        if (sh.ov_el[i] && pos != sh.ov_added && better(e, pos, br.err, br.pos)) br = Best{e, pos};
       }
       __syncwarp();
     }
@@ -1805,10 +1801,10 @@ struct MsgPath {
       ov_scan_a(off, card, n0, __ldg(a.points + 3 * (int64_t)pos) * inv_r,
                 __ldg(a.points + 3 * (int64_t)pos + 1) * inv_r, __ldg(a.points + 3 * (int64_t)pos + 2) * inv_r);
       bar_ov();
-      ov_eligibility(card);
     }
     if (threadIdx.x == 0) {
       sh.ov_res = res;
+      sh.ov_added = pos;
       sh.ov_n = n;
       sh.ov_bits = phase_bits;
       sh.cm.dbl[5] = p2;
