@@ -1,7 +1,9 @@
 #!/bin/bash
 # Round-end measurement set (run on the GPU box from the repo root):
 # default bench line, the reference (CPU) arm, every BASELINE config, the
-# configs[4] m-sweep. Outputs under gpurun_out/.
+# configs[4] m-sweep, then the ncu evidence (launch list of the default bench
+# command, full captures of the loop and volume kernels on configs[1] and of
+# the grid loop kernel on configs[2]). Outputs under gpurun_out/.
 set -u
 mkdir -p gpurun_out
 timeout 900 python bench.py > gpurun_out/m_bench_cfg1.json 2> gpurun_out/m_bench_cfg1.err
@@ -11,3 +13,13 @@ timeout 900 python bench.py --config 2 --steps 5 --warmup 3 --no-cpu-baseline > 
 timeout 1500 python bench.py --config 3 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/m_bench_cfg3.json 2> gpurun_out/m_bench_cfg3.err
 timeout 900 python tools/msweep.py --out gpurun_out/m_msweep.json > gpurun_out/m_msweep.log 2>&1
 for f in gpurun_out/m_bench_*.json; do echo "$f: $(head -c 160 $f)"; done
+if [ "${NCU:-1}" = 1 ]; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file gpurun_out/m_launches_cfg1.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline \
+      > gpurun_out/m_ncu_launches.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gcb_msg_kernel|eval_kernel" \
+      -s 0 -c 2 -o gpurun_out/m_prof_cfg1 python tools/prof_step.py --steps 1 > gpurun_out/m_ncu_cfg1.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gcb_grid_kernel" \
+      -s 0 -c 1 -o gpurun_out/m_prof_cfg2 python tools/prof_step.py --config 2 --steps 1 > gpurun_out/m_ncu_cfg2.log 2>&1
+  tail -1 gpurun_out/m_ncu_cfg1.log gpurun_out/m_ncu_cfg2.log
+fi
