@@ -21,5 +21,5 @@ if [ "${NCU:-1}" = 1 ]; then
       -s 0 -c 2 -o gpurun_out/m_prof_cfg1 python tools/prof_step.py --steps 1 > gpurun_out/m_ncu_cfg1.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gcb_grid_kernel" \
       -s 0 -c 1 -o gpurun_out/m_prof_cfg2 python tools/prof_step.py --config 2 --steps 1 > gpurun_out/m_ncu_cfg2.log 2>&1
-  tail -1 gpurun_out/m_ncu_cfg1.log gpurun_out/m_ncu_cfg2.log
+  tail -n 1 gpurun_out/m_ncu_cfg1.log gpurun_out/m_ncu_cfg2.log
 fi
