@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <cstdio>
 
 #include "rbf_common.cuh"
 #include "rbf_internal.h"
@@ -269,14 +270,20 @@ extern "C" int rbf_eval(const double* targets, int64_t n_targets, const double* 
 // targets streamed in `chunks` pieces so the host->device copy of piece k+1
 // and the device->host copy of piece k-1 overlap the kernel on piece k (PCIe
 // is full duplex: 48 MB each way in 1.0 ms together vs 0.87 ms alone). The
-// copy streams and events are the library's own (created once per device);
-// the kernels run on `stream`, which also waits for the last copy, so the
-// caller synchronises `stream` before reading `host_out`. Per-target results
+// copy and kernel streams and the events are the library's own (created
+// once per device and host thread); they start after the work pending on
+// `stream`, and `stream` waits for the last copy, so the caller synchronises
+// `stream` before reading `host_out`. Per-target results
 // are bitwise those of one rbf_eval launch.
 namespace {
+// Chunk kernels rotate over kPipeCompute library-owned streams so the
+// partial last wave of chunk k runs beside the first wave of chunk k+1 (one
+// stream serialises them: 8 chunks of 250k targets cost 8 full-wave times).
+constexpr int kPipeCompute = 3;
 struct PipeStreams {
   int device = -1;
   cudaStream_t in = nullptr, out = nullptr;
+  cudaStream_t comp[kPipeCompute] = {};
   cudaEvent_t ev[3 * 64] = {};
 };
 }  // namespace
@@ -297,6 +304,7 @@ extern "C" int rbf_eval_host(const double* host_targets, int64_t n_targets, cons
   if (ps.device != dev) {
     RBF_CUDA_TRY(cudaStreamCreateWithFlags(&ps.in, cudaStreamNonBlocking));
     RBF_CUDA_TRY(cudaStreamCreateWithFlags(&ps.out, cudaStreamNonBlocking));
+    for (auto& c : ps.comp) RBF_CUDA_TRY(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
     for (auto& e : ps.ev) RBF_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ps.device = dev;
   }
@@ -305,21 +313,75 @@ extern "C" int rbf_eval_host(const double* host_targets, int64_t n_targets, cons
   RBF_CUDA_TRY(cudaEventRecord(ps.ev[0], compute));
   RBF_CUDA_TRY(cudaStreamWaitEvent(ps.in, ps.ev[0], 0));
   RBF_CUDA_TRY(cudaStreamWaitEvent(ps.out, ps.ev[0], 0));
-  int64_t step = (n_targets + chunks - 1) / chunks;
-  step = (step + 511) / 512 * 512;
-  int c = 0;
-  for (int64_t lo = 0; lo < n_targets; lo += step, ++c) {
-    const int64_t cnt = std::min(step, n_targets - lo);
+  for (auto& cs : ps.comp) RBF_CUDA_TRY(cudaStreamWaitEvent(cs, ps.ev[0], 0));
+  // Chunk schedule: chunks - 1 equal pieces, then the last one halved
+  // `tail` times (1/2, 1/4, .., the rest), so what runs after the final
+  // host->device copy -- the last kernel (its CTAs alone on their SMs) and
+  // the last device->host copy -- is a small piece.
+  constexpr int64_t kBlock = 768;  // targets per volume-kernel CTA (128 x 6)
+  static const int tail = [] {
+    const char* e = getenv("RBF_PIPE_TAIL");
+    return e ? atoi(e) : 2;
+  }();
+  int64_t sizes[63];
+  int nchunks = 0;
+  {
+    int64_t step = (n_targets + chunks - 1) / chunks;
+    step = (step + kBlock - 1) / kBlock * kBlock;
+    int64_t lo = 0;
+    while (lo < n_targets && nchunks < 63) {
+      int64_t rest = n_targets - lo, cnt = std::min(step, rest);
+      if (rest <= step) {  // the last piece: split it
+        for (int t = 0; t < tail && nchunks < 62 && rest > 2 * kBlock; ++t) {
+          const int64_t half = (rest / 2 + kBlock - 1) / kBlock * kBlock;
+          sizes[nchunks++] = half;
+          lo += half;
+          rest -= half;
+        }
+        cnt = rest;
+      }
+      sizes[nchunks++] = cnt;
+      lo += cnt;
+    }
+  }
+  // RBF_PIPE_TRACE=1 (diagnostic): per-chunk device timeline on stderr
+  static const bool trace = getenv("RBF_PIPE_TRACE") != nullptr;
+  cudaEvent_t tev[4 * 63 + 1] = {};
+  if (trace) {
+    for (auto& e : tev) RBF_CUDA_TRY(cudaEventCreate(&e));
+    RBF_CUDA_TRY(cudaEventRecord(tev[0], compute));
+  }
+  int64_t lo = 0;
+  for (int c = 0; c < nchunks; lo += sizes[c], ++c) {
+    const int64_t cnt = sizes[c];
     cudaEvent_t in_done = ps.ev[3 * c + 1], k_done = ps.ev[3 * c + 2];
+    cudaStream_t cs = ps.comp[c % kPipeCompute];
     RBF_CUDA_TRY(cudaMemcpyAsync(dev_in + 3 * lo, host_targets + 3 * lo, 24 * cnt, cudaMemcpyHostToDevice, ps.in));
     RBF_CUDA_TRY(cudaEventRecord(in_done, ps.in));
-    RBF_CUDA_TRY(cudaStreamWaitEvent(compute, in_done, 0));
+    RBF_CUDA_TRY(cudaStreamWaitEvent(cs, in_done, 0));
     const int rc = rbf_eval(dev_in + 3 * lo, cnt, sup_points, sup_weights, n_sup, radius, deform,
-                            dev_out + 3 * lo, stream);
+                            dev_out + 3 * lo, cs);
     if (rc != RBF_OK) return rc;
-    RBF_CUDA_TRY(cudaEventRecord(k_done, compute));
+    RBF_CUDA_TRY(cudaEventRecord(k_done, cs));
     RBF_CUDA_TRY(cudaStreamWaitEvent(ps.out, k_done, 0));
     RBF_CUDA_TRY(cudaMemcpyAsync(host_out + 3 * lo, dev_out + 3 * lo, 24 * cnt, cudaMemcpyDeviceToHost, ps.out));
+    if (trace) {
+      RBF_CUDA_TRY(cudaEventRecord(tev[4 * c + 1], ps.in));
+      RBF_CUDA_TRY(cudaEventRecord(tev[4 * c + 2], cs));
+      RBF_CUDA_TRY(cudaEventRecord(tev[4 * c + 3], ps.out));
+    }
+  }
+  if (trace) {
+    RBF_CUDA_TRY(cudaDeviceSynchronize());
+    for (int c = 0; c < nchunks; ++c) {
+      float h = 0.f, k = 0.f, d = 0.f;
+      cudaEventElapsedTime(&h, tev[0], tev[4 * c + 1]);
+      cudaEventElapsedTime(&k, tev[0], tev[4 * c + 2]);
+      cudaEventElapsedTime(&d, tev[0], tev[4 * c + 3]);
+      fprintf(stderr, "pipe chunk %d n=%lld h2d_end %.3f kernel_end %.3f d2h_end %.3f ms\n", c,
+              (long long)sizes[c], h, k, d);
+    }
+    for (auto& e : tev) cudaEventDestroy(e);
   }
   RBF_CUDA_TRY(cudaEventRecord(ps.ev[3 * 63 + 2], ps.out));
   RBF_CUDA_TRY(cudaStreamWaitEvent(compute, ps.ev[3 * 63 + 2], 0));

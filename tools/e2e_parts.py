@@ -43,7 +43,7 @@ print("deform_points (pageable) %.3f ms" % timed(lambda: P.deform_points(vol_pag
 sp, sw = torch.from_numpy(sup.points).cuda(), torch.from_numpy(sup.weights).cuda()
 out = torch.empty_like(vol_d)
 print("eval_device (resident)  %.3f ms" % timed(lambda: P.eval_device(vol_d, sp, sw, wl.radius, deform=True, out=out)))
-for chunks in (4, 8, 16, 32):
+for chunks in (4, 6, 8, 12, 16, 24, 32):
     C._PIPELINE_CHUNKS = chunks
     print("pipelined, %2d chunks    %.3f ms" % (chunks, timed(lambda: P.deform_points(vol, sup, wl.radius))))
 h = torch.empty((wl.nv, 3), dtype=torch.float64, pin_memory=True)
