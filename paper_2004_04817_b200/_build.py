@@ -53,7 +53,9 @@ def build(force=False, verbose=False):
             cmd = [os.environ.get("CXX", "g++"), *CXX_FLAGS, "-I", cuda_inc, "-c", str(CSRC / src),
                    "-o", str(obj)]
         else:
-            cmd = [_nvcc(), *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+            # RBF_NVCC_EXTRA: extra flags for experiments (e.g. -DRBF_DEBUG_CAND)
+            cmd = [_nvcc(), *NVCC_FLAGS, *os.environ.get("RBF_NVCC_EXTRA", "").split(), "-c",
+                   str(CSRC / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
