@@ -197,6 +197,8 @@ typedef struct rbf_gcb_state {
 /* rbf_gcb_args.flags */
 #define RBF_GCB_PHASES 1
 #define RBF_GCB_NO_OVERLAP 2 /* MSG path: no next-group scan during appends (A/B tests) */
+#define RBF_GCB_NO_TAIL 4    /* one-cluster paths: final sweep in the cluster instead of a
+                                stream-ordered whole-GPU tail launch (A/B tests) */
 
 /* Launch shapes of the selection kernel:
  *  MSG     one 16-CTA cluster, n < 384: the factor rows (owner-stable, row
@@ -246,8 +248,11 @@ typedef struct rbf_gcb_args {
   size_t scratch_bytes;
 } rbf_gcb_args;
 
-/* CTAs the selection kernel uses in `mode` for a problem of nb nodes and
- * m groups (mode AUTO picks cluster or grid). */
+/* Team width to size the selection scratch for (rbf_gcb_scratch_bytes):
+ * the SM count in every mode, since a one-cluster launch is followed by a
+ * whole-GPU launch for its final sweep and a run can move between shapes;
+ * *resolved_mode_host is the shape `mode` resolves to (AUTO picks MSG for
+ * group sizes up to 2048, GRID above). */
 RBF_API int rbf_gcb_ctas(int32_t mode, int32_t nb, int32_t m, int32_t* ctas_host,
                          int32_t* resolved_mode_host);
 RBF_API size_t rbf_gcb_scratch_bytes(int32_t nb, int32_t cap, int32_t ctas);

@@ -24,6 +24,7 @@ RBF_ESTALL = 6
 RBF_EPARSE = 7
 GCB_PHASES = 1  # rbf_gcb_args.flags: record per-phase SM cycles
 GCB_NO_OVERLAP = 2  # rbf_gcb_args.flags: MSG path without the overlapped next-group scan
+GCB_NO_TAIL = 4  # rbf_gcb_args.flags: one-cluster final sweep without the whole-GPU tail launch
 STATUS_DONE = 1
 GCB_AUTO = 0
 GCB_CLUSTER = 1

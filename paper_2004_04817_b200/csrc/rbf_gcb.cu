@@ -57,6 +57,10 @@ constexpr int64_t kClusterScanPairs = 400000;  // per group scan, see gcb_driver
 constexpr int64_t kSmemScanPairs = 150000;
 constexpr int kMsgDefaultClusters = 1;         // MSG path: clusters sharing the scans
 constexpr int kNone = 0x7fffffff;
+// internal rbf_gcb_args.flags bits (set by rbf_gcb_run on its own copy)
+constexpr int kFlagTailSweep = 1 << 16;  // one-cluster launch: stop before the final sweep,
+                                         // which a whole-GPU tail launch runs
+constexpr int kFlagTailOnly = 1 << 17;   // that tail launch: final sweep of a finished loop only
 
 struct LoopScratch {
   unsigned* bar;   // grid barrier word
@@ -2202,8 +2206,14 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
     }
   };
 
-  gather_groups(a, s);
-  P.begin(n);
+  // the tail launch after a one-cluster loop: proceed only if that loop
+  // finished and handed its final sweep over (else the host decides)
+  const bool tail = (a.flags & kFlagTailOnly) != 0;
+  if (tail && !(done_loop && __ldcg(&st->status) == RBF_EGROW && __ldcg(&st->want_mode) == RBF_GCB_GRID)) return;
+  if (!tail) {  // the final sweep reads neither the group order nor the column copy
+    gather_groups(a, s);
+    P.begin(n);
+  }
   P.sync();
 
   if (n == 0) {
@@ -2343,7 +2353,13 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
     gk = gk + 1 == m ? 0 : gk + 1;
   }
 
-  // final verification sweep (selection.py:388-412), natural order
+  // final verification sweep (selection.py:388-412), natural order: one
+  // cluster's 16 SMs would take Nb x n pairs at 1/9 of the GPU, so the
+  // one-cluster paths hand it to the tail launch queued behind them
+  if ((a.flags & kFlagTailSweep) && self_mode != RBF_GCB_GRID) {
+    save(RBF_EGROW, RBF_GCB_GRID);
+    return;
+  }
   if (nrec >= a.rec_cap) {
     save(RBF_EGROW, self_mode);
     return;
@@ -2469,7 +2485,7 @@ extern "C" int rbf_gcb_ctas(int32_t mode, int32_t nb, int32_t m, int32_t* ctas_h
   const int sms = sm_count(dev);
   if (sms <= 0) return set_error(RBF_ECUDA, "no CUDA device");
   // scratch is sized for the widest team so a run can switch paths
-  if (ctas_host) *ctas_host = r == RBF_GCB_GRID ? sms : kClusterCTAs;
+  if (ctas_host) *ctas_host = sms;
   if (resolved_mode_host) *resolved_mode_host = r;
   return RBF_OK;
 }
@@ -2518,7 +2534,11 @@ extern "C" int rbf_gcb_run(const rbf_gcb_args* args, void* stream) {
   cudaStream_t st = as_stream(stream);
   RBF_CUDA_TRY(cudaMemsetAsync(s.bar, 0, 64, st));
   rbf_gcb_args acopy = a;
+  acopy.flags &= 0xffff;
   const bool ph = (a.flags & RBF_GCB_PHASES) != 0;
+  // one-cluster paths: the final sweep runs in a whole-GPU launch queued
+  // right behind (it returns at once unless the loop finished)
+  const bool tail = (mode == RBF_GCB_MSG || mode == RBF_GCB_SMEM) && !(a.flags & RBF_GCB_NO_TAIL);
   if (mode == RBF_GCB_MSG) {
     int dev = 0;
     RBF_CUDA_TRY(cudaGetDevice(&dev));
@@ -2526,9 +2546,11 @@ extern "C" int rbf_gcb_run(const rbf_gcb_args* args, void* stream) {
     int ncl = a.clusters > 0 ? a.clusters : kMsgDefaultClusters;
     ncl = ncl < 1 ? 1 : (ncl > max_cl ? max_cl : (ncl > 16 ? 16 : ncl));
     RBF_CUDA_TRY(cudaMemsetAsync(s.xseq, 0, sizeof(unsigned) * 2 * 16, st));
+    if (tail) acopy.flags |= kFlagTailSweep;
     RBF_CUDA_TRY(launch_cluster(ph ? (const void*)gcb_msg_kernel<true> : (const void*)gcb_msg_kernel<false>,
                                 acopy, s, sizeof(MsgShared), st, ncl));
   } else if (mode == RBF_GCB_SMEM) {
+    if (tail) acopy.flags |= kFlagTailSweep;
     RBF_CUDA_TRY(launch_cluster(ph ? (const void*)gcb_smem_kernel<true> : (const void*)gcb_smem_kernel<false>,
                                 acopy, s, sizeof(SmemShared), st));
   } else if (mode == RBF_GCB_CLUSTER) {
@@ -2565,6 +2587,25 @@ extern "C" int rbf_gcb_run(const rbf_gcb_args* args, void* stream) {
     cfg.attrs = attrs;
     cfg.numAttrs = nattr;
     RBF_CUDA_TRY(cudaLaunchKernelEx(&cfg, grid_kernel, acopy, s));
+  }
+  if (tail) {
+    rbf_gcb_args t = a;
+    t.flags = (a.flags & 0xffff) | kFlagTailOnly;
+    t.mode = RBF_GCB_GRID;
+    const size_t smem = sizeof(GlobalShared);
+    auto grid_kernel = ph ? gcb_grid_kernel<true> : gcb_grid_kernel<false>;
+    RBF_CUDA_TRY(cudaFuncSetAttribute(grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeCooperative;
+    at.val.cooperative = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(kLoopThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    RBF_CUDA_TRY(cudaLaunchKernelEx(&cfg, grid_kernel, t, s));
   }
   return RBF_OK;
 }

@@ -545,6 +545,8 @@ def _gcb_run(boundary, config, mode=None, phases=None):
     args.flags = N.GCB_PHASES if phases else 0
     if os.environ.get("RBF_GCB_OVERLAP", "1") == "0":  # A/B: no next-group scan during appends
         args.flags |= N.GCB_NO_OVERLAP
+    if os.environ.get("RBF_GCB_TAIL", "1") == "0":  # A/B: final sweep inside the one-cluster launch
+        args.flags |= N.GCB_NO_TAIL
     args.radius = radius
     args.tol = float(config.tol)
     args.dup_dist = NEAR_DUPLICATE_FRACTION * config.radius
@@ -559,7 +561,9 @@ def _gcb_run(boundary, config, mode=None, phases=None):
         args.state = buf.state.data_ptr()
         args.scratch, args.scratch_bytes = buf.scratch.data_ptr(), buf.scratch_bytes
         used_grid = used_grid or args.mode == N.GCB_GRID
-        with N.launching("rbf_gcb_run", kernels=1):
+        # one-cluster shapes queue a whole-GPU tail launch for the final sweep
+        tail = args.mode in (N.GCB_MSG, N.GCB_SMEM) and not (args.flags & N.GCB_NO_TAIL)
+        with N.launching("rbf_gcb_run", kernels=2 if tail else 1):
             rc = lib.rbf_gcb_run(N.ctypes.byref(args), stream)
         N.check(rc, "rbf_gcb_run")
         # state, selection, weights and records in one staged read (the kernel

@@ -470,6 +470,34 @@ def test_selection_overlapped_scan_on_off(cuda, monkeypatch, name):
     assert np.abs(lm["1"] - lm["0"]).max() <= 1e-12 * lm["0"].max()
 
 
+@pytest.mark.parametrize("name", ["cfg1_m32", "cfg0_m8", "smooth3_m5"])
+@pytest.mark.parametrize("mode", ["msg", "smem"])
+def test_selection_tail_sweep_on_off(cuda, monkeypatch, name, mode):
+    """One-cluster paths with the final sweep in the whole-GPU tail launch
+    queued behind them (default) and inside the cluster (RBF_GCB_TAIL=0):
+    the same sequence and records as the reference, the same final-sweep
+    record, maxima equal to rounding."""
+    from paper_2004_04817_b200 import _native as N
+    from paper_2004_04817_b200.selection import _gcb_run
+
+    g = load_golden(name)
+    pts, disp, _ = golden_inputs(name, g)
+    radius, tol, cap, m, seed = g["params"]
+    b = cuda.BoundarySet(np.arange(len(pts)), pts, disp)
+    cfg = cuda.SelectionConfig(radius=radius, tol=tol, max_supports=int(cap), m=int(m), seed=int(seed))
+    fin = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("RBF_GCB_TAIL", flag)
+        res = _gcb_run(b, cfg, mode={"msg": N.GCB_MSG, "smem": N.GCB_SMEM}[mode])
+        assert np.array_equal(res.support.nodes, g["seq"]), flag
+        assert [r.node for r in res.history.records] == g["rec_node"].tolist(), flag
+        f = res.history.final_sweep
+        assert [f.iteration, f.node, f.kernel_evals, f.cum_kernel_evals] == g["final"].tolist(), flag
+        assert res.converged == bool(f.local_max_error <= tol)
+        fin[flag] = f.local_max_error
+    assert fin["1"] == pytest.approx(fin["0"], rel=1e-7, abs=1e-16)
+
+
 def test_resolve_auto_m_matches_reference_golden(cuda):
     """--m auto's greedy probe + error-decay extrapolation (reference
     cli.py:69-99) picks the reference's m."""

@@ -1,6 +1,7 @@
 """Time the volume-kernel launch variants (RBF_EVAL_VARIANT) on configs[1]:
-2M targets x 287 supports. One subprocess per variant (the variant is read
-once per process)."""
+2M targets x 287 supports (or `--nv N --nc C`: the first N volume points,
+C supports). One subprocess per variant (the variant is read once per
+process)."""
 import json
 import os
 import subprocess
@@ -13,9 +14,10 @@ import paper_2004_04817_b200 as P
 from paper_2004_04817_b200 import workloads as W
 wl = W.config(1)
 rng = np.random.default_rng(0)
-idx = rng.choice(wl.nb, 287, replace=False)
-sp = torch.from_numpy(wl.points[idx]).cuda(); sw = torch.from_numpy(rng.normal(size=(287, 3)) * 0.01).cuda()
-vol = torch.from_numpy(wl.volume).cuda(); out = torch.empty_like(vol)
+NV, NC = int(sys.argv[1]), int(sys.argv[2])
+idx = rng.choice(wl.nb, NC, replace=False)
+sp = torch.from_numpy(wl.points[idx]).cuda(); sw = torch.from_numpy(rng.normal(size=(NC, 3)) * 0.01).cuda()
+vol = torch.from_numpy(wl.volume[:NV]).cuda(); out = torch.empty_like(vol)
 for _ in range(3): P.eval_device(vol, sp, sw, 2.0, deform=True, out=out)
 torch.cuda.synchronize()
 best = 1e9
@@ -25,12 +27,15 @@ for _ in range(10):
     best = min(best, e0.elapsed_time(e1))
 print(best)
 '''
+args = sys.argv[1:]
+NV = int(args[args.index("--nv") + 1]) if "--nv" in args else 2_000_000
+NC = int(args[args.index("--nc") + 1]) if "--nc" in args else 287
 res = {}
 for v in range(10):
     env = dict(os.environ, RBF_EVAL_VARIANT=str(v))
-    r = subprocess.run([sys.executable, "-c", CODE], env=env, capture_output=True, text=True)
+    r = subprocess.run([sys.executable, "-c", CODE, str(NV), str(NC)], env=env, capture_output=True, text=True)
     ms = float(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else None
-    tf = 22 * 2_000_000 * 287 / (ms * 1e-3) / 1e12 if ms else None
+    tf = 22 * NV * NC / (ms * 1e-3) / 1e12 if ms else None
     res[v] = {"ms": ms, "tflops": tf, "err": r.stderr[-300:] if r.returncode else ""}
     print(v, res[v], flush=True)
 print(json.dumps(res))
