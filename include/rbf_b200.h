@@ -185,7 +185,8 @@ typedef struct rbf_gcb_state {
   int32_t final_pos;
   int32_t fault;        /* watchdog flag                                   */
   int32_t want_mode;    /* on RBF_EGROW: mode the kernel asks to resume in  */
-  int32_t pad_;
+  int32_t handover;     /* on RBF_EGROW to GRID: 0, or the one-cluster mode whose
+                           run without appends the whole-GPU tail launch resolves */
   /* diagnostics: SM cycles CTA 0 spent per phase, summed over the run:
    * [0] scan+barrier, [1] fold+row, [2] c0, [3] r, [4] c, [5] pivot+cols,
    * [6] bookkeeping, [7] seeds, [8] final sweep, [9] appends, [10] iterations,

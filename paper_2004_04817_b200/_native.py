@@ -70,7 +70,7 @@ class GcbState(ctypes.Structure):
         ("final_pos", ctypes.c_int32),
         ("fault", ctypes.c_int32),
         ("want_mode", ctypes.c_int32),
-        ("pad_", ctypes.c_int32),
+        ("handover", ctypes.c_int32),
         ("phase_cycles", ctypes.c_double * 16),
     ]
 

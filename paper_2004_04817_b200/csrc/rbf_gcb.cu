@@ -61,6 +61,12 @@ constexpr int kNone = 0x7fffffff;
 constexpr int kFlagTailSweep = 1 << 16;  // one-cluster launch: stop before the final sweep,
                                          // which a whole-GPU tail launch runs
 constexpr int kFlagTailOnly = 1 << 17;   // that tail launch: final sweep of a finished loop only
+// one-cluster paths: after this many consecutive groups within tolerance
+// (and m >= 2x it) the rest of the run is resolved by the tail launch from
+// one whole-boundary pass (the weights do not change until an append)
+constexpr int kStreakHandover = 8;
+constexpr int kFlagResumeOnly = 1 << 18;  // a second one-cluster launch queued behind the tail:
+                                          // runs only if the state asks to resume in its shape
 
 struct LoopScratch {
   unsigned* bar;   // grid barrier word
@@ -2191,8 +2197,9 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
   const int m = a.m;
   int par = 0;
 
-  auto save = [&](int status, int want_mode) {
+  auto save = [&](int status, int want_mode, int handover = 0) {
     if (leader) {
+      st->handover = handover;
       for (int i = 0; i < 16; ++i) st->phase_cycles[i] += cm.phase[i];
       st->n = n;
       st->k = k;
@@ -2209,8 +2216,16 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
   // the tail launch after a one-cluster loop: proceed only if that loop
   // finished and handed its final sweep over (else the host decides)
   const bool tail = (a.flags & kFlagTailOnly) != 0;
-  if (tail && !(done_loop && __ldcg(&st->status) == RBF_EGROW && __ldcg(&st->want_mode) == RBF_GCB_GRID)) return;
-  if (!tail) {  // the final sweep reads neither the group order nor the column copy
+  const int handover = tail ? __ldcg(&st->handover) : 0;
+  if (tail && !((done_loop || handover) && __ldcg(&st->status) == RBF_EGROW &&
+                __ldcg(&st->want_mode) == RBF_GCB_GRID))
+    return;
+  // the one-cluster launch queued behind the tail: continue only where the
+  // tail handed a run back (or any pause that asks for this shape)
+  if ((a.flags & kFlagResumeOnly) &&
+      !(__ldcg(&st->status) == RBF_EGROW && __ldcg(&st->want_mode) == self_mode))
+    return;
+  if (!tail) {  // the final sweep and the run resolution read neither the group order nor the column copy
     gather_groups(a, s);
     P.begin(n);
   }
@@ -2243,8 +2258,75 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
     t2_carry = 0.0;
   }
 
-  const int card_max = (a.nb + m - 1) / m;
   int gk = k % m;
+  if (tail && handover && !done_loop) {
+    // A run of groups within tolerance handed over by a one-cluster launch:
+    // the weights stay fixed until the next append, so one whole-boundary
+    // pass gives every following group's (max error, lowest position); the
+    // groups are then taken in order exactly as the loop below would, until
+    // the run reaches m (loop done: the final sweep follows) or a group
+    // exceeds the tolerance (hand back: the one-cluster launch rescans it
+    // and appends). The pass time is the first resolved record's t1.
+    const uint64_t t_a = leader_timer();
+    P.scan(nullptr, a.points, a.disp, a.nb, n, par);
+    P.gather(par, 1);
+    par ^= 1;
+    Best* gbest = reinterpret_cast<Best*>(s.gpt);  // 24 nb bytes >= 16 m
+    for (int g = blockIdx.x; g < m; g += gridDim.x) {
+      const int lo = P.group_off(g), hi = P.group_off(g + 1);
+      Best b{-1.0, kNone};
+      for (int t = lo + (int)threadIdx.x; t < hi; t += kLoopThreads) {
+        const int pos = __ldg(a.group_pos + t);
+        const double e = __ldcg(s.err + pos);
+        if (better(e, pos, b.err, b.pos)) b = Best{e, pos};
+      }
+      b = cta_best(cm, b, 0);
+      if (threadIdx.x == 0) gbest[g] = b;
+      __syncthreads();
+    }
+    P.sync();
+    const uint64_t t_b = leader_timer();
+    bool first = true;
+    while (true) {
+      if (nrec >= a.rec_cap) {
+        save(RBF_EGROW, handover);
+        return;
+      }
+      const Best gb{__ldcg(&gbest[gk].err), __ldcg(&gbest[gk].pos)};
+      if (gb.err > a.tol) {  // the run ends here: back to the one-cluster loop
+        save(RBF_EGROW, handover);
+        return;
+      }
+      if (leader) {
+        rbf_gcb_record rec;
+        rec.group = gk;
+        rec.node_pos = gb.pos;
+        rec.added = 0;
+        rec.n_before = n;
+        rec.local_max = gb.err;
+        rec.t1_s = first ? (double)(t_b - t_a) * 1e-9 : 0.0;
+        rec.t2_s = t2_carry;
+        a.records[nrec] = rec;
+      }
+      first = false;
+      nrec += 1;
+      t2_carry = 0.0;
+      streak_noadd += 1;
+      streak_ok += 1;
+      if (streak_ok >= m) {
+        done_loop = 1;
+        break;
+      }
+      if (streak_noadd >= m) {
+        save(RBF_ESTALL, self_mode);
+        return;
+      }
+      k += 1;
+      gk = gk + 1 == m ? 0 : gk + 1;
+    }
+  }
+
+  const int card_max = (a.nb + m - 1) / m;
   int ov_group = -1;  // group whose scan ran during the last append (MsgPath)
   while (!done_loop) {
     if (n >= a.max_supports) {
@@ -2345,6 +2427,12 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
         save(RBF_ESTALL, self_mode);
         return;
       }
+      if ((a.flags & kFlagTailSweep) && self_mode != RBF_GCB_GRID && streak_ok >= kStreakHandover &&
+          m >= 2 * kStreakHandover) {  // likely the closing run: the tail launch resolves it
+        k += 1;
+        save(RBF_EGROW, RBF_GCB_GRID, self_mode);
+        return;
+      }
     } else {
       streak_noadd = 0;
       streak_ok = 0;
@@ -2431,6 +2519,30 @@ __global__ void __launch_bounds__(kLoopThreads, 1) gcb_msg_kernel(rbf_gcb_args a
   gcb_driver(P, a, s, pc, RBF_GCB_MSG);
   P.finish();
   P.tmem_free();
+}
+
+// The whole-GPU launch queued behind a one-cluster launch: the final sweep of
+// a finished loop, or the resolution of a run of groups within tolerance
+// (gcb_driver); it returns at once otherwise.
+static cudaError_t launch_tail(const rbf_gcb_args& a, LoopScratch& s, int ctas, bool ph, cudaStream_t st) {
+  rbf_gcb_args t = a;
+  t.flags = (a.flags & 0xffff) | kFlagTailOnly;
+  t.mode = RBF_GCB_GRID;
+  const size_t smem = sizeof(GlobalShared);
+  auto grid_kernel = ph ? gcb_grid_kernel<true> : gcb_grid_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute at;
+  at.id = cudaLaunchAttributeCooperative;
+  at.val.cooperative = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(kLoopThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = &at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, grid_kernel, t, s);
 }
 
 static int resolve_mode(int mode, int nb, int m) {
@@ -2539,20 +2651,32 @@ extern "C" int rbf_gcb_run(const rbf_gcb_args* args, void* stream) {
   // one-cluster paths: the final sweep runs in a whole-GPU launch queued
   // right behind (it returns at once unless the loop finished)
   const bool tail = (mode == RBF_GCB_MSG || mode == RBF_GCB_SMEM) && !(a.flags & RBF_GCB_NO_TAIL);
-  if (mode == RBF_GCB_MSG) {
-    int dev = 0;
-    RBF_CUDA_TRY(cudaGetDevice(&dev));
-    const int max_cl = sm_count(dev) / kClusterCTAs;
-    int ncl = a.clusters > 0 ? a.clusters : kMsgDefaultClusters;
-    ncl = ncl < 1 ? 1 : (ncl > max_cl ? max_cl : (ncl > 16 ? 16 : ncl));
-    RBF_CUDA_TRY(cudaMemsetAsync(s.xseq, 0, sizeof(unsigned) * 2 * 16, st));
+  // with runs handed to the tail (m >= 2 kStreakHandover), a second
+  // one-cluster launch and a second tail are queued too, so a run that ends
+  // in an append resumes without a host round trip
+  const int rounds = tail && a.m >= 2 * kStreakHandover ? 2 : 1;
+  if (mode == RBF_GCB_MSG || mode == RBF_GCB_SMEM) {
+    int ncl = 1;
+    if (mode == RBF_GCB_MSG) {
+      int dev = 0;
+      RBF_CUDA_TRY(cudaGetDevice(&dev));
+      const int max_cl = sm_count(dev) / kClusterCTAs;
+      ncl = a.clusters > 0 ? a.clusters : kMsgDefaultClusters;
+      ncl = ncl < 1 ? 1 : (ncl > max_cl ? max_cl : (ncl > 16 ? 16 : ncl));
+      RBF_CUDA_TRY(cudaMemsetAsync(s.xseq, 0, sizeof(unsigned) * 2 * 16, st));
+    }
     if (tail) acopy.flags |= kFlagTailSweep;
-    RBF_CUDA_TRY(launch_cluster(ph ? (const void*)gcb_msg_kernel<true> : (const void*)gcb_msg_kernel<false>,
-                                acopy, s, sizeof(MsgShared), st, ncl));
-  } else if (mode == RBF_GCB_SMEM) {
-    if (tail) acopy.flags |= kFlagTailSweep;
-    RBF_CUDA_TRY(launch_cluster(ph ? (const void*)gcb_smem_kernel<true> : (const void*)gcb_smem_kernel<false>,
-                                acopy, s, sizeof(SmemShared), st));
+    for (int r = 0; r < rounds; ++r) {
+      rbf_gcb_args x = acopy;
+      if (r > 0) x.flags |= kFlagResumeOnly;
+      if (mode == RBF_GCB_MSG)
+        RBF_CUDA_TRY(launch_cluster(ph ? (const void*)gcb_msg_kernel<true> : (const void*)gcb_msg_kernel<false>,
+                                    x, s, sizeof(MsgShared), st, ncl));
+      else
+        RBF_CUDA_TRY(launch_cluster(ph ? (const void*)gcb_smem_kernel<true> : (const void*)gcb_smem_kernel<false>,
+                                    x, s, sizeof(SmemShared), st));
+      if (tail) RBF_CUDA_TRY(launch_tail(a, s, ctas, ph, st));
+    }
   } else if (mode == RBF_GCB_CLUSTER) {
     RBF_CUDA_TRY(launch_cluster(ph ? (const void*)gcb_cluster_kernel<true> : (const void*)gcb_cluster_kernel<false>,
                                 acopy, s, sizeof(GlobalShared), st));
@@ -2587,25 +2711,6 @@ extern "C" int rbf_gcb_run(const rbf_gcb_args* args, void* stream) {
     cfg.attrs = attrs;
     cfg.numAttrs = nattr;
     RBF_CUDA_TRY(cudaLaunchKernelEx(&cfg, grid_kernel, acopy, s));
-  }
-  if (tail) {
-    rbf_gcb_args t = a;
-    t.flags = (a.flags & 0xffff) | kFlagTailOnly;
-    t.mode = RBF_GCB_GRID;
-    const size_t smem = sizeof(GlobalShared);
-    auto grid_kernel = ph ? gcb_grid_kernel<true> : gcb_grid_kernel<false>;
-    RBF_CUDA_TRY(cudaFuncSetAttribute(grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cudaLaunchAttribute at;
-    at.id = cudaLaunchAttributeCooperative;
-    at.val.cooperative = 1;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ctas);
-    cfg.blockDim = dim3(kLoopThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cfg.attrs = &at;
-    cfg.numAttrs = 1;
-    RBF_CUDA_TRY(cudaLaunchKernelEx(&cfg, grid_kernel, t, s));
   }
   return RBF_OK;
 }
