@@ -195,7 +195,8 @@ __global__ void best_reduce_kernel(const Best* __restrict__ partials, int n, dou
 // threads x 6 targets), 1-5 the difference form at several geometries
 // (threads, targets per thread, support tile, min resident blocks), 6 the
 // expanded form at 128 x 4, 7-8 the difference form at 64 x 6 (6 CTAs per
-// SM; support tile 128 / 64), 9 the expanded form at 64 x 6. RBF_EVAL_VARIANT selects one for experiments
+// SM; support tile 128 / 64), 9 the expanded form at 64 x 6, 10-11 short-grid shapes
+// (128 x 2 and 64 x 4: more CTAs when the targets fill less than one wave). RBF_EVAL_VARIANT selects one for experiments
 // (tools/eval_variants.py).
 template <int MODE, int NT, int TPT, int TILE, int MINB>
 static void launch_eval_variant(const double* targets, int64_t n, const double* sp, const double* sw,
@@ -228,6 +229,8 @@ static void launch_eval(int variant, const double* t, int64_t n, const double* s
     case 7: launch_eval_variant<MODE, 64, 6, 128, 6>(t, n, sp, sw, ns, inv_r, out, s); break;
     case 8: launch_eval_variant<MODE, 64, 6, 64, 6>(t, n, sp, sw, ns, inv_r, out, s); break;
     case 9: launch_expanded<MODE, 64, 6, 128, 6>(t, n, sp, sw, ns, inv_r, out, s); break;
+    case 10: launch_eval_variant<MODE, 128, 2, 128, 8>(t, n, sp, sw, ns, inv_r, out, s); break;
+    case 11: launch_eval_variant<MODE, 64, 4, 128, 6>(t, n, sp, sw, ns, inv_r, out, s); break;
     default: launch_eval_variant<MODE, 128, 4, 128, 4>(t, n, sp, sw, ns, inv_r, out, s); break;
   }
 }
