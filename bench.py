@@ -7,11 +7,18 @@ A step is the reference's hot path on one batch of synthetic input
 (BASELINE.json configs[C], default C = 1: Nb = 20,000 wing nodes,
 Nv = 2,000,000 volume nodes, GCB m = 32, R = 2, tol = 1e-4 max|d|, FP64):
 the full selection loop including the final sweep (device resident)
-followed by deform_points over all Nv volume nodes. With N > 1 GPUs
-(torchrun): configs 0-1 run N independent replicas (weak scaling; they are
-too small to shard); configs 2-3 run the selection on rank 0,
-broadcast the support set (NCCL) and shard the volume (strong scaling).
-`--multi` overrides the choice.
+followed by deform_points over all Nv volume nodes.
+
+N > 1 GPUs: one process per GPU. Without WORLD_SIZE in the environment,
+``--gpus N`` re-launches itself under ``torch.distributed.run`` with N
+ranks (127.0.0.1); under torchrun WORLD_SIZE must equal N. The default
+multi-GPU step is the sharded one north_star describes (``--multi shard``,
+strong scaling: the whole job is one selection + one Nv volume): the loop
+runs on rank 0, the support set is broadcast (NCCL), the final sweep and the
+volume are split into contiguous shards; ``volume_ms`` is
+the volume stage's max over ranks and ``volume_speedup`` divides the
+one-GPU volume time (measured in the same run on rank 0) by it.
+``--multi replicas`` runs N independent whole steps instead (weak scaling).
 
 Metric: RBF pair-evaluations per second, whole job, with
 pairs = sum_i card(G_i) * Nc(i) + Nb * Nc   (selection, = cum_kernel_evals)
@@ -22,7 +29,9 @@ inside the timed region. L2 (126 MB) is flushed between timed steps by
 writing a 256 MiB buffer. Rank 0 prints ONE JSON line on stdout.
 
 --impl reference times the reference algorithm on the host CPU (the oracle
-port in oracle/, all host cores) on a bounded sample of the same workload.
+port in oracle/, all host cores): per step the full selection loop plus a
+strided sample of the volume, the volume time scaled to all Nv targets, so
+its pairs/s is quoted on the same pair mix as the GPU arm.
 """
 
 import argparse
@@ -32,6 +41,7 @@ import statistics
 import subprocess
 import sys
 import time
+from dataclasses import replace
 from pathlib import Path
 
 import numpy as np
@@ -53,10 +63,9 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=100_000, help="volume targets in the CPU sample")
-    ap.add_argument("--multi", choices=["auto", "replicas", "shard"], default="auto",
-                    help="N > 1: independent replicas (weak scaling; auto for configs 0-1, too small "
-                         "to shard, SURVEY.md 8(e)) or selection on rank 0 + volume sharded (strong; "
-                         "auto for configs 2-3)")
+    ap.add_argument("--multi", choices=["shard", "replicas"], default="shard",
+                    help="N > 1: selection on rank 0 + final sweep and volume sharded over the ranks "
+                         "(default, strong scaling) or N independent whole steps (weak scaling)")
     return ap.parse_args()
 
 
@@ -74,17 +83,31 @@ def workload(cfg):
 
 
 def multi_mode(args, world):
-    if world == 1:
-        return "single"
-    if args.multi != "auto":
-        return args.multi
-    return "replicas" if args.config in (0, 1) else "shard"
+    return "single" if world == 1 else args.multi
+
+
+def relaunch(args):
+    """``--gpus N`` outside torchrun: run this script under
+    torch.distributed.run with N ranks, one per GPU (127.0.0.1)."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(REPO / "bench.py"), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def tol_frac(wl):
+    return wl.tol / float(np.linalg.norm(wl.disp, axis=1).max())
 
 
 def config_desc(wl, world, extra=None, mode="single"):
     d = {
-        "workload": f"BASELINE configs[{wl.name[-1]}]: {wl.name} wing, Nb={wl.nb}, Nv={wl.nv}, "
-                    f"GCB m={wl.m}, R={wl.radius}, tol=1e-4*max|d|, seed={wl.seed}",
+        "workload": f"BASELINE configs[{wl.name[-1]}]: {wl.name}, Nb={wl.nb}, Nv={wl.nv}, "
+                    f"GCB m={wl.m}, R={wl.radius}, tol={tol_frac(wl):.0e}*max|d|, seed={wl.seed}",
         "nb": wl.nb,
         "nv": wl.nv,
         "m": wl.m,
@@ -93,7 +116,7 @@ def config_desc(wl, world, extra=None, mode="single"):
         "parallelism": ("1 GPU" if mode == "single" else
                         f"{world} independent replicas (each GPU runs the whole step)"
                         if mode == "replicas" else
-                        f"selection on rank 0, volume sharded over {world} GPUs"),
+                        f"selection loop on rank 0; final sweep and volume sharded over {world} GPUs"),
         "l2": "flushed between timed steps (256 MiB write)",
     }
     if extra:
@@ -211,9 +234,25 @@ def load_traffic():
 
 
 # ---------------------------------------------------------- CPU baseline
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
 def cpu_oracle_step(wl, threads, sample):
-    """One bounded CPU step of the reference algorithm (oracle port):
-    the full selection loop + a strided sample of the volume evaluation."""
+    """One CPU step of the reference algorithm (the oracle port, numpy/scipy/
+    OpenBLAS with the reference's own thread pool of ``threads`` workers):
+    the full selection loop, then a strided ``sample`` of the volume whose
+    time is scaled to all Nv targets (per-target cost is uniform: every
+    target walks all Nc supports, reference core.py:301-334). The step's
+    pairs are the GPU arm's: A_sel + Nv * Nc."""
     sys.path.insert(0, str(REPO / "oracle"))
     import rbf_oracle as O
 
@@ -225,9 +264,10 @@ def cpu_oracle_step(wl, threads, sample):
     t2 = time.perf_counter()
     nc = len(out["seq"])
     sel_pairs = sum(r[4] for r in out["records"]) + out["final"][3]
-    pairs = sel_pairs + len(idx) * nc
-    return {"pairs": pairs, "seconds": t2 - t0, "select_s": t1 - t0, "volume_s": t2 - t1,
-            "nc": nc, "sample": len(idx)}
+    vol_s = (t2 - t1) * wl.nv / len(idx)
+    return {"pairs": sel_pairs + wl.nv * nc, "seconds": (t1 - t0) + vol_s, "select_s": t1 - t0,
+            "volume_sample_s": t2 - t1, "volume_s": vol_s, "nc": nc, "sample": len(idx),
+            "selection_pairs": sel_pairs, "wall_s": t2 - t0}
 
 
 def host_threads():
@@ -235,6 +275,12 @@ def host_threads():
         return len(os.sched_getaffinity(0))
     except AttributeError:
         return os.cpu_count() or 1
+
+
+def cpu_sample_desc(wl, s, threads):
+    return (f"full selection loop (Nb={wl.nb}, m={wl.m}, {s['select_s']:.2f} s) + {s['sample']} of {wl.nv} "
+            f"volume targets ({s['volume_sample_s']:.2f} s, scaled x{wl.nv / s['sample']:.0f} to all Nv), "
+            f"oracle port of the reference (numpy/scipy/OpenBLAS), {threads} thread(s), {cpu_model()}")
 
 
 def run_reference(args, rank, world):
@@ -248,20 +294,26 @@ def run_reference(args, rank, world):
     pairs = sum(s["pairs"] for s in steps)
     secs = sum(s["seconds"] for s in steps)
     value = pairs / secs
-    sample = (f"full selection loop (Nb={wl.nb}, m={wl.m}) + {steps[0]['sample']} of {wl.nv} "
-              f"volume targets per step, oracle port of the reference (numpy/scipy/OpenBLAS)")
+    one = cpu_oracle_step(wl, 1, args.cpu_sample)  # the workers = 1 leg
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": secs / len(steps) * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak" if multi_mode(args, world) == "replicas" else "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, "
+                                                      "paper_2004_04817_b200/workloads.py)",
         "impl": "reference",
-        "config": config_desc(wl, 1, {"parallelism": f"CPU, {threads} threads"}),
+        "config": config_desc(wl, world, mode=multi_mode(args, world)),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": cpu_sample_desc(wl, steps[0], threads), "cpu_model": cpu_model()},
+        "cpu_baseline_1_worker": {"value": one["pairs"] / one["seconds"], "unit": UNIT, "cores": 1,
+                                  "kind": "port", "ms_per_step": one["seconds"] * 1e3,
+                                  "sample": cpu_sample_desc(wl, one, 1)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "breakdown": {"select_s": statistics.mean(s["select_s"] for s in steps),
-                      "volume_sample_s": statistics.mean(s["volume_s"] for s in steps),
-                      "nc": steps[0]["nc"]},
+                      "volume_s": statistics.mean(s["volume_s"] for s in steps),
+                      "volume_sample_s": statistics.mean(s["volume_sample_s"] for s in steps),
+                      "nc": steps[0]["nc"], "selection_pairs": steps[0]["selection_pairs"],
+                      "volume_pairs": wl.nv * steps[0]["nc"]},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -278,7 +330,8 @@ def run_ours(args, rank, world, local):
 
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group(os.environ.get("RBF_BENCH_BACKEND", "nccl"),
+                                device_id=torch.device("cuda", local))
     N.require_cuda()
 
     def barrier():
@@ -289,27 +342,31 @@ def run_ours(args, rank, world, local):
     peak = measure_fp64_peak()
     mode = multi_mode(args, world)
     replicas = mode == "replicas"
+    shard = mode == "shard"
     boundary = P.stage_boundary(P.BoundarySet(np.arange(wl.nb), wl.points, wl.disp))
+    bpts, bdisp = boundary._device[2], boundary._device[3]
     cfg = P.SelectionConfig(radius=wl.radius, tol=wl.tol, max_supports=wl.nb, m=wl.m, seed=wl.seed)
-    lo, hi = (0, wl.nv) if replicas else multi.shard_range(wl.nv, rank, world)
+    lo, hi = multi.shard_range(wl.nv, rank, world) if shard else (0, wl.nv)
     nv_local = hi - lo
     vol_d = torch.from_numpy(np.ascontiguousarray(wl.volume[lo:hi])).cuda()
     out_d = torch.empty_like(vol_d)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    from paper_2004_04817_b200.selection import _gcb_run
 
-    def select_and_share():
-        if replicas or rank == 0:
+    def device_step():
+        """One step on device-resident inputs; returns (result or None, Nc)."""
+        if not shard:
             res = P.gcb_select(boundary, cfg)
             sp = torch.from_numpy(res.support.points).cuda()
             sw = torch.from_numpy(res.support.weights).cuda()
         else:
-            res, sp, sw = None, None, torch.empty((0, 3), dtype=torch.float64, device="cuda")
-        if world > 1 and not replicas:
-            sp, sw = multi.broadcast_support(sp, sw)
-        return res, sp, sw
-
-    def device_step():
-        res, sp, sw = select_and_share()
+            res = _gcb_run(boundary, cfg, sweep=False) if rank == 0 else None
+            sp, sw, _ = (multi.broadcast_support(res.support.points, res.support.weights) if rank == 0
+                         else multi.broadcast_support(None, None))
+            sweep = multi.sweep(bpts, bdisp, sp, sw, wl.radius)
+            if res is not None:
+                res.history.final_sweep = replace(res.history.final_sweep, node=int(sweep.pos),
+                                                  local_max_error=sweep.max_error)
         P.eval_device(vol_d, sp, sw, wl.radius, deform=True, out=out_d)
         return res, sp.shape[0]
 
@@ -319,7 +376,7 @@ def run_ours(args, rank, world, local):
 
     clocks = ClockSampler(local)
     clocks.start()
-    times, logs, nc, a_sel = [], [], None, None
+    times, logs, nc, a_sel, res = [], [], None, None, None
     for _ in range(args.steps):
         flush.zero_()
         barrier()
@@ -327,14 +384,15 @@ def run_ours(args, rank, world, local):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with N.launch_log(timing=True) as log:
             e0.record()
-            res, nc = device_step()
+            r, nc = device_step()
             e1.record()
         torch.cuda.synchronize()
         barrier()
         times.append(e0.elapsed_time(e1) * 1e-3)
         logs.append(log)
-        if res is not None:
-            a_sel = res.history.final_sweep.cum_kernel_evals
+        if r is not None:
+            res = r
+            a_sel = r.history.final_sweep.cum_kernel_evals
     # e2e through the public API: host (pinned) buffers in and out
     vol_host_t = torch.from_numpy(np.ascontiguousarray(wl.volume[lo:hi])).pin_memory()
     vol_host = vol_host_t.numpy()
@@ -344,16 +402,8 @@ def run_ours(args, rank, world, local):
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        if replicas or rank == 0:
-            res2 = P.gcb_select(P.BoundarySet(np.arange(wl.nb), wl.points, wl.disp), cfg)
-            sup = res2.support
-        if world > 1 and not replicas:
-            if rank == 0:
-                sp2, sw2 = torch.from_numpy(sup.points).cuda(), torch.from_numpy(sup.weights).cuda()
-            else:
-                sp2, sw2 = None, torch.empty((0, 3), dtype=torch.float64, device="cuda")
-            sp2, sw2 = multi.broadcast_support(sp2, sw2)
-            sup = P.SupportSet(np.arange(sp2.shape[0]), sp2.cpu().numpy(), sw2.cpu().numpy())
+        b_host = P.BoundarySet(np.arange(wl.nb), wl.points, wl.disp)
+        sup = (multi.gcb_select(b_host, cfg) if shard else P.gcb_select(b_host, cfg)).support
         moved = P.deform_points(vol_host, sup, wl.radius)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
@@ -367,23 +417,47 @@ def run_ours(args, rank, world, local):
     # with the phase clock on (it costs ~4 % of the loop, so the timed runs
     # leave it off)
     prof_hist = None
-    if rank == 0 or replicas:
-        from paper_2004_04817_b200.selection import _gcb_run
-
+    if rank == 0:
         prof_hist = _gcb_run(boundary, cfg, phases=True).history
+
+    # volume stage alone: this rank's shard (max over ranks) and, on rank 0,
+    # the whole Nv on one GPU, for the volume-stage speed-up
+    sp_d = torch.from_numpy(np.ascontiguousarray(sup.points)).cuda()
+    sw_d = torch.from_numpy(np.ascontiguousarray(sup.weights)).cuda()
+
+    def time_eval(v, o, reps=5):
+        best = []
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            P.eval_device(v, sp_d, sw_d, wl.radius, deform=True, out=o)
+            e1.record()
+            torch.cuda.synchronize()
+            best.append(e0.elapsed_time(e1))
+        return statistics.median(best)
+
+    barrier()
+    vol_shard_ms = time_eval(vol_d, out_d)
+    vol_full_ms = None
+    if world > 1 and shard and rank == 0:
+        del out_d
+        full_d = torch.from_numpy(wl.volume).cuda()
+        vol_full_ms = time_eval(full_d, torch.empty_like(full_d), reps=3)
+        del full_d
 
     # ---- aggregate (max over ranks) ----
     t_local = float(sum(times))
     e2e_local = float(sum(e2e_times))
     if world > 1:
-        tt = torch.tensor([t_local, e2e_local], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([t_local, e2e_local, vol_shard_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_total, e2e_total = tt.tolist()
+        t_total, e2e_total, vol_shard_max = tt.tolist()
         a = torch.tensor([a_sel or 0], dtype=torch.int64, device="cuda")
         dist.broadcast(a, src=0)
         a_sel = int(a.item())
     else:
-        t_total, e2e_total = t_local, e2e_local
+        t_total, e2e_total, vol_shard_max = t_local, e2e_local, vol_shard_ms
     pairs_per_step = (a_sel + wl.nv * nc) * (world if replicas else 1)
     value = pairs_per_step * args.steps / t_total
     e2e_value = pairs_per_step * args.steps / e2e_total
@@ -393,6 +467,7 @@ def run_ours(args, rank, world, local):
     # a switch of storage path), the volume one
     sel_ms = [sum(lg.kernel_ms("rbf_gcb_run")) for lg in logs if lg.kernel_ms("rbf_gcb_run")]
     vol_ms = [sum(lg.kernel_ms("rbf_eval")) for lg in logs if lg.kernel_ms("rbf_eval")]
+    sweep_ms = [sum(lg.kernel_ms("rbf_errors_argmax")) for lg in logs if lg.kernel_ms("rbf_errors_argmax")]
     launches = sum(lg.count for lg in logs) / len(logs)
     launches_sel = sum(lg.by_name.get("rbf_gcb_run", 0) for lg in logs) / len(logs)
     traffic = {k: v.get("bytes_per_launch") for k, v in load_traffic().items()}
@@ -400,11 +475,12 @@ def run_ours(args, rank, world, local):
     kernels = []
     if sel_ms:
         t = statistics.mean(sel_ms) * 1e-3
-        ach = FLOP_PER_PAIR * a_sel / t / 1e12
+        sel_pairs = a_sel - (wl.nb * nc if shard and world > 1 else 0)
+        ach = FLOP_PER_PAIR * sel_pairs / t / 1e12
         kernels.append({"kernel": "gcb_*_kernel (selection loop, launches per step: %d)"
                                   % round(launches_sel), "ms": t * 1e3,
-                        "bound": "latency (grid barriers) / fp64", "achieved": ach, "peak": peak_tf,
-                        "unit": "TFLOP/s", "frac": ach / peak_tf,
+                        "bound": "latency (dependent DSMEM hops / grid barriers)", "achieved": ach,
+                        "peak": peak_tf, "unit": "TFLOP/s", "frac": ach / peak_tf,
                         "traffic": traffic.get("gcb_kernel")})
     if vol_ms:
         t = statistics.mean(vol_ms) * 1e-3
@@ -412,15 +488,21 @@ def run_ours(args, rank, world, local):
         kernels.append({"kernel": "eval_kernel<deform> (volume)", "ms": t * 1e3, "bound": "fp64",
                         "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s", "frac": ach / peak_tf,
                         "traffic": traffic.get("eval_kernel")})
-    dominant = max(kernels, key=lambda k: k["ms"]) if kernels else None
+    if sweep_ms:
+        kernels.append({"kernel": "rbf_errors_argmax_dev (sharded final sweep, this rank's slice)",
+                        "ms": statistics.mean(sweep_ms)})
+    dominant = max((k for k in kernels if "frac" in k), key=lambda k: k["ms"]) if kernels else None
 
-    cpu = None
+    cpu = cpu1 = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = host_threads()
         s = cpu_oracle_step(wl, threads, args.cpu_sample)
         cpu = {"value": s["pairs"] / s["seconds"], "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"full selection loop + {s['sample']} of {wl.nv} volume targets, oracle "
-                         f"port (numpy/scipy/OpenBLAS, {threads} threads), {s['seconds']:.2f} s"}
+               "ms_per_step": s["seconds"] * 1e3, "sample": cpu_sample_desc(wl, s, threads),
+               "cpu_model": cpu_model()}
+        s1 = cpu_oracle_step(wl, 1, args.cpu_sample)
+        cpu1 = {"value": s1["pairs"] / s1["seconds"], "unit": UNIT, "cores": 1, "kind": "port",
+                "ms_per_step": s1["seconds"] * 1e3, "sample": cpu_sample_desc(wl, s1, 1)}
 
     if rank == 0:
         h2d = (wl.nb * 48 + wl.nb * 4 + (wl.m + 1) * 4 + nv_local * 24 + nc * 48)
@@ -446,8 +528,11 @@ def run_ours(args, rank, world, local):
             "kernels": kernels,
             "fp64_peak": peak,
             "cpu_baseline": cpu,
+            "cpu_baseline_1_worker": cpu1,
             "clocks": clocks.summary(),
             "gpu_launches": launches,
+            "volume_ms": vol_shard_max,
+            "volume_ms_source": "volume kernel alone on this rank's shard, median of 5, max over ranks",
             "breakdown": {"nc": nc, "selection_pairs": a_sel, "volume_pairs": wl.nv * nc,
                           "iterations": len(res.history.records),
                           # the reference's per-stage columns (cli.py:38), device clock:
@@ -456,7 +541,7 @@ def run_ours(args, rank, world, local):
                           "t2_ms": 1e3 * sum(r.t2_s for r in res.history.records),
                           "selection_ms": statistics.mean(sel_ms) if sel_ms else None,
                           "volume_ms": statistics.mean(vol_ms) if vol_ms else None,
-                          "converged": bool(res.converged),
+                          "converged": bool(res.converged) if res.converged is not None else None,
                           "loop_mode": getattr(res.history, "device_mode", None),
                           "loop_phase_us": {k: v / 1.965e3 for k, v in
                                             getattr(prof_hist, "device_phase_cycles", {}).items()
@@ -465,6 +550,9 @@ def run_ours(args, rank, world, local):
                           "loop_counts": {k: getattr(prof_hist, "device_phase_cycles", {}).get(k)
                                           for k in ("appends", "iterations")}},
         }
+        if vol_full_ms is not None:
+            line["volume_ms_1gpu"] = vol_full_ms
+            line["volume_speedup"] = vol_full_ms / vol_shard_max
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -475,6 +563,11 @@ def run_ours(args, rank, world, local):
 def main():
     args = parse_args()
     rank, world, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch(args)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args, rank, world)
     return run_ours(args, rank, world, local)

@@ -104,6 +104,25 @@ RBF_API int rbf_errors_argmax(const double* bnd_points, const double* bnd_disp,
                       double radius, double* err_out, double* best_host,
                       void* scratch, size_t scratch_bytes, void* stream);
 
+/* Device-resident variant for sharded sweeps (multi-GPU final sweep and
+ * error_summary): no synchronisation; `best_dev` (device,
+ * 2 doubles) receives {max_err, pos_of_max + pos_offset}, the rank's 16-byte
+ * record for the all-gather. n_targets == 0 (an empty shard) writes the
+ * neutral record {-1, INT32_MAX}. The per-row summation order is the one
+ * rbf_errors_argmax uses for the same (n_targets, n_sup).
+ */
+RBF_API int rbf_errors_argmax_dev(const double* bnd_points, const double* bnd_disp,
+                          const int64_t* positions, int64_t n_targets,
+                          const double* sup_points, const double* sup_weights, int64_t n_sup,
+                          double radius, double* err_out, int64_t pos_offset, double* best_dev,
+                          void* scratch, size_t scratch_bytes, void* stream);
+
+/* Fold n (err, pos) records (n x 2 doubles, device) into out[2] (device):
+ * the largest error, exact ties to the lowest position (selection.py:231-234).
+ * The combine step of a sharded sweep after the all-gather of the per-rank
+ * records. */
+RBF_API int rbf_best_fold(const double* recs, int64_t n, double* out, void* stream);
+
 /* ---------------------------------------------------------------------
  * Nearest-support distances.  Replaces metrics.py:45-48
  * `_nearest_distances` (cdist + row min, used by kl_divergence
@@ -200,6 +219,9 @@ typedef struct rbf_gcb_state {
 #define RBF_GCB_NO_OVERLAP 2 /* MSG path: no next-group scan during appends (A/B tests) */
 #define RBF_GCB_NO_TAIL 4    /* one-cluster paths: final sweep in the cluster instead of a
                                 stream-ordered whole-GPU tail launch (A/B tests) */
+#define RBF_GCB_NO_SWEEP 8   /* end the loop without the final sweep (state->final_pos = -1,
+                                no final record): the caller sweeps the boundary itself, e.g.
+                                sharded over GPUs with rbf_errors_argmax_dev + rbf_best_fold */
 
 /* Launch shapes of the selection kernel:
  *  MSG     one 16-CTA cluster, n < 384: the factor rows (owner-stable, row

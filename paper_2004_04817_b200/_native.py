@@ -25,6 +25,7 @@ RBF_EPARSE = 7
 GCB_PHASES = 1  # rbf_gcb_args.flags: record per-phase SM cycles
 GCB_NO_OVERLAP = 2  # rbf_gcb_args.flags: MSG path without the overlapped next-group scan
 GCB_NO_TAIL = 4  # rbf_gcb_args.flags: one-cluster final sweep without the whole-GPU tail launch
+GCB_NO_SWEEP = 8  # rbf_gcb_args.flags: end the loop without the final sweep (the caller sweeps)
 STATUS_DONE = 1
 GCB_AUTO = 0
 GCB_CLUSTER = 1
@@ -126,6 +127,10 @@ SIGNATURES = [
     ("rbf_errors_argmax", ctypes.c_int,
      [c_dp, c_dp, c_dp, ctypes.c_int64, c_dp, c_dp, ctypes.c_int64, ctypes.c_double, c_dp,
       ctypes.POINTER(ctypes.c_double), c_dp, ctypes.c_size_t, c_dp]),
+    ("rbf_errors_argmax_dev", ctypes.c_int,
+     [c_dp, c_dp, c_dp, ctypes.c_int64, c_dp, c_dp, ctypes.c_int64, ctypes.c_double, c_dp,
+      ctypes.c_int64, c_dp, c_dp, ctypes.c_size_t, c_dp]),
+    ("rbf_best_fold", ctypes.c_int, [c_dp, ctypes.c_int64, c_dp, c_dp]),
     ("rbf_nearest", ctypes.c_int, [c_dp, ctypes.c_int64, c_dp, ctypes.c_int64, c_dp, c_dp]),
     ("rbf_chol_scratch_bytes", ctypes.c_size_t, [ctypes.c_int64]),
     ("rbf_chol_append", ctypes.c_int,

@@ -176,7 +176,8 @@ eval_expanded_kernel(const double* __restrict__ tpts, int64_t nt, const double* 
 }
 
 // One block folds the per-block (err, pos) partials in block order.
-__global__ void best_reduce_kernel(const Best* __restrict__ partials, int n, double* __restrict__ result) {
+__global__ void best_reduce_kernel(const Best* __restrict__ partials, int n, double* __restrict__ result,
+                                   int64_t pos_offset) {
   Best b{-1.0, 0x7fffffff};
   for (int i = threadIdx.x; i < n; i += blockDim.x) b = best_of(b, partials[i]);
   b = warp_best(b);
@@ -187,7 +188,43 @@ __global__ void best_reduce_kernel(const Best* __restrict__ partials, int n, dou
     Best r = s[0];
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = best_of(r, s[w]);
     result[0] = r.err;
-    result[1] = (double)r.pos;
+    result[1] = (double)(r.pos + pos_offset);
+  }
+}
+
+// Fold of n (err, pos) records (pos held exactly as a double), larger error
+// first, exact ties to the lowest position: the combine step of a sharded
+// sweep (one record per rank, all-gathered) -- reference selection.py:231-234.
+__global__ void best_fold_kernel(const double* __restrict__ recs, int64_t n, double* __restrict__ out) {
+  double be = -1.0, bp = 0.0;
+  bool have = false;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double e = recs[2 * i], p = recs[2 * i + 1];
+    if (!have || e > be || (e == be && p < bp)) {
+      be = e;
+      bp = p;
+      have = true;
+    }
+  }
+  __shared__ double s_e[256], s_p[256];
+  __shared__ bool s_h[256];
+  s_e[threadIdx.x] = be;
+  s_p[threadIdx.x] = bp;
+  s_h[threadIdx.x] = have;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    bool h = false;
+    double e0 = -1.0, p0 = -1.0;
+    for (int t = 0; t < (int)blockDim.x; ++t) {
+      if (!s_h[t]) continue;
+      if (!h || s_e[t] > e0 || (s_e[t] == e0 && s_p[t] < p0)) {
+        e0 = s_e[t];
+        p0 = s_p[t];
+        h = true;
+      }
+    }
+    out[0] = e0;
+    out[1] = p0;
   }
 }
 
@@ -505,11 +542,10 @@ extern "C" size_t rbf_errors_scratch_bytes(int64_t n_targets) {
   return bytes;
 }
 
-extern "C" int rbf_errors_argmax(const double* bnd_points, const double* bnd_disp,
-                                 const int64_t* positions, int64_t n_targets,
-                                 const double* sup_points, const double* sup_weights, int64_t n_sup,
-                                 double radius, double* err_out, double* best_host, void* scratch,
-                                 size_t scratch_bytes, void* stream) {
+static int errors_argmax(const double* bnd_points, const double* bnd_disp, const int64_t* positions,
+                         int64_t n_targets, const double* sup_points, const double* sup_weights, int64_t n_sup,
+                         double radius, double* err_out, double* best_host, double* best_dev,
+                         int64_t pos_offset, void* scratch, size_t scratch_bytes, void* stream) {
   if (n_targets <= 0) return set_error(RBF_EARG, "group is empty");
   if (!(radius > 0.0)) return set_error(RBF_EARG, "radius must be positive, got %g", radius);
   if (n_sup > INT32_MAX || n_targets > INT32_MAX) return set_error(RBF_EARG, "size too large");
@@ -518,7 +554,7 @@ extern "C" int rbf_errors_argmax(const double* bnd_points, const double* bnd_dis
     return set_error(RBF_EARG, "scratch too small");
   int64_t nblk = 0;
   cudaStream_t s = as_stream(stream);
-  double* result = reinterpret_cast<double*>(scratch);
+  double* result = best_dev ? best_dev : reinterpret_cast<double*>(scratch);
   Best* partials = reinterpret_cast<Best*>(static_cast<char*>(scratch) + 256);
   const double inv_r = 1.0 / radius;
   const int S = split_slices(n_targets, n_sup);
@@ -543,12 +579,43 @@ extern "C" int rbf_errors_argmax(const double* bnd_points, const double* bnd_dis
         partials);
     RBF_LAUNCH_CHECK("eval_kernel<error>");
   }
-  best_reduce_kernel<<<1, 256, 0, s>>>(partials, (int)nblk, result);
+  best_reduce_kernel<<<1, 256, 0, s>>>(partials, (int)nblk, result, pos_offset);
   RBF_LAUNCH_CHECK("best_reduce_kernel");
   if (best_host) {
     RBF_CUDA_TRY(cudaMemcpyAsync(best_host, result, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     RBF_CUDA_TRY(cudaStreamSynchronize(s));
   }
+  return RBF_OK;
+}
+
+extern "C" int rbf_errors_argmax(const double* bnd_points, const double* bnd_disp,
+                                 const int64_t* positions, int64_t n_targets,
+                                 const double* sup_points, const double* sup_weights, int64_t n_sup,
+                                 double radius, double* err_out, double* best_host, void* scratch,
+                                 size_t scratch_bytes, void* stream) {
+  return errors_argmax(bnd_points, bnd_disp, positions, n_targets, sup_points, sup_weights, n_sup, radius,
+                       err_out, best_host, nullptr, 0, scratch, scratch_bytes, stream);
+}
+
+extern "C" int rbf_errors_argmax_dev(const double* bnd_points, const double* bnd_disp,
+                                     const int64_t* positions, int64_t n_targets,
+                                     const double* sup_points, const double* sup_weights, int64_t n_sup,
+                                     double radius, double* err_out, int64_t pos_offset, double* best_dev,
+                                     void* scratch, size_t scratch_bytes, void* stream) {
+  if (!best_dev) return set_error(RBF_EARG, "null pointer");
+  if (n_targets == 0) {  // an empty shard contributes the neutral record {-1, INT32_MAX}
+    best_reduce_kernel<<<1, 256, 0, as_stream(stream)>>>(nullptr, 0, best_dev, 0);
+    RBF_LAUNCH_CHECK("best_reduce_kernel");
+    return RBF_OK;
+  }
+  return errors_argmax(bnd_points, bnd_disp, positions, n_targets, sup_points, sup_weights, n_sup, radius,
+                       err_out, nullptr, best_dev, pos_offset, scratch, scratch_bytes, stream);
+}
+
+extern "C" int rbf_best_fold(const double* recs, int64_t n, double* out, void* stream) {
+  if (n <= 0 || !recs || !out) return set_error(RBF_EARG, "rbf_best_fold: empty input or null pointer");
+  best_fold_kernel<<<1, 256, 0, as_stream(stream)>>>(recs, n, out);
+  RBF_LAUNCH_CHECK("best_fold_kernel");
   return RBF_OK;
 }
 

@@ -2259,6 +2259,9 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
   }
 
   int gk = k % m;
+  // the tail's whole-boundary pass is still valid when its run closes the loop
+  // (same weights): the final sweep then folds its per-group bests
+  const Best* swept = nullptr;
   if (tail && handover && !done_loop) {
     // A run of groups within tolerance handed over by a one-cluster launch:
     // the weights stay fixed until the next append, so one whole-boundary
@@ -2315,6 +2318,7 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
       streak_ok += 1;
       if (streak_ok >= m) {
         done_loop = 1;
+        swept = gbest;
         break;
       }
       if (streak_noadd >= m) {
@@ -2441,6 +2445,16 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
     gk = gk + 1 == m ? 0 : gk + 1;
   }
 
+  // RBF_GCB_NO_SWEEP: the caller runs the final sweep itself (multi-GPU: one
+  // boundary shard per rank, multi.py); the loop ends here
+  if (a.flags & RBF_GCB_NO_SWEEP) {
+    if (leader) {
+      st->final_max = -1.0;
+      st->final_pos = -1;
+    }
+    save(1, self_mode);
+    return;
+  }
   // final verification sweep (selection.py:388-412), natural order: one
   // cluster's 16 SMs would take Nb x n pairs at 1/9 of the GPU, so the
   // one-cluster paths hand it to the tail launch queued behind them
@@ -2454,11 +2468,23 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
   }
   const uint64_t t_a = leader_timer();
   pc.mark(6);
-  P.scan(nullptr, a.points, a.disp, a.nb, n, par);
-  P.gather(par, 1);
-  par ^= 1;
+  Best bu{-1.0, kNone};
+  if (swept) {  // the groups partition the boundary: the best group best is the sweep's
+    if (blockIdx.x == 0) {
+      Best b{-1.0, kNone};
+      for (int g = tid; g < m; g += kLoopThreads) {
+        const Best q{__ldcg(&swept[g].err), __ldcg(&swept[g].pos)};
+        if (better(q.err, q.pos, b.err, b.pos)) b = q;
+      }
+      bu = cta_best(cm, b, 0);
+    }
+  } else {
+    P.scan(nullptr, a.points, a.disp, a.nb, n, par);
+    P.gather(par, 1);
+    par ^= 1;
+    bu = cm.bcast[0];
+  }
   pc.mark(8);
-  const Best bu = cm.bcast[0];
   const uint64_t t_b = leader_timer();
   if (leader) {
     rbf_gcb_record rec;

@@ -504,7 +504,11 @@ def gcb_select(boundary, config):
     return _gcb_run(boundary, config)
 
 
-def _gcb_run(boundary, config, mode=None, phases=None):
+def _gcb_run(boundary, config, mode=None, phases=None, sweep=True):
+    """The device loop. ``sweep=False`` stops before the final sweep
+    (RBF_GCB_NO_SWEEP; multi.gcb_select shards it over ranks): the returned
+    history's ``final_sweep`` then carries the iteration number, counters and
+    t2 but ``node`` = -1 and a NaN maximum, and ``converged`` is None."""
     nb = len(boundary)
     m = config.m
     if not 1 <= m <= nb:
@@ -547,6 +551,8 @@ def _gcb_run(boundary, config, mode=None, phases=None):
         args.flags |= N.GCB_NO_OVERLAP
     if os.environ.get("RBF_GCB_TAIL", "1") == "0":  # A/B: final sweep inside the one-cluster launch
         args.flags |= N.GCB_NO_TAIL
+    if not sweep:
+        args.flags |= N.GCB_NO_SWEEP
     args.radius = radius
     args.tol = float(config.tol)
     args.dup_dist = NEAR_DUPLICATE_FRACTION * config.radius
@@ -608,7 +614,7 @@ def _gcb_run(boundary, config, mode=None, phases=None):
     sizes = np.diff(off)
     history = SelectionHistory(seed=config.seed, m=m)
     idx = boundary.indices
-    body = recs[:-1]
+    body = recs[:-1] if sweep else recs
     groups = body["group"].astype(np.int64)
     evals = sizes[groups] * body["n_before"].astype(np.int64)
     cum = np.cumsum(evals)
@@ -616,26 +622,32 @@ def _gcb_run(boundary, config, mode=None, phases=None):
     history.records = _RecordList((
         range(3, 3 + len(body)), groups.tolist(), nodes.tolist(), body["local_max"].tolist(),
         evals.tolist(), cum.tolist(), body["t1_s"].tolist(), body["t2_s"].tolist()))
-    fin = recs[-1]
     sweep_evals = nb * n
     total = (int(cum[-1]) if len(cum) else 0) + sweep_evals
-    history.final_sweep = IterationRecord(
-        iteration=st.k + 1,
-        group=-1,
-        node=int(idx[fin["node_pos"]]),
-        local_max_error=float(fin["local_max"]),
-        kernel_evals=sweep_evals,
-        cum_kernel_evals=total,
-        t1_s=float(fin["t1_s"]),
-        t2_s=float(fin["t2_s"]),
-    )
+    if sweep:
+        fin = recs[-1]
+        history.final_sweep = IterationRecord(
+            iteration=st.k + 1,
+            group=-1,
+            node=int(idx[fin["node_pos"]]),
+            local_max_error=float(fin["local_max"]),
+            kernel_evals=sweep_evals,
+            cum_kernel_evals=total,
+            t1_s=float(fin["t1_s"]),
+            t2_s=float(fin["t2_s"]),
+        )
+    else:  # the caller sweeps (multi.gcb_select)
+        history.final_sweep = IterationRecord(
+            iteration=st.k + 1, group=-1, node=-1, local_max_error=float("nan"),
+            kernel_evals=sweep_evals, cum_kernel_evals=total, t1_s=0.0, t2_s=float(st.t2_carry))
     # diagnostics: SM cycles of CTA 0 per phase of the device loop
     history.device_phase_cycles = dict(zip(N.PHASES, list(st.phase_cycles))) if phases else {}
     history.device_mode = {N.GCB_CLUSTER: "cluster", N.GCB_GRID: "grid", N.GCB_SMEM: "smem",
                            N.GCB_MSG: "msg"}[args.mode]
     support = SupportSet(nodes=idx[sel], points=boundary.points[sel], weights=weights)
     return SelectionResult(
-        support=support, history=history, converged=float(fin["local_max"]) <= config.tol
+        support=support, history=history,
+        converged=(float(fin["local_max"]) <= config.tol) if sweep else None,
     )
 
 

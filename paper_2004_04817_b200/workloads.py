@@ -173,26 +173,30 @@ def wing_body(nb=200_000, nv=40_000_000, seed=0, m=64, radius=4.0, tol_frac=1e-4
     """Config 3: fuselage + wing + pylon + nacelle, points split by area.
 
     Fuselage: cylinder r = 0.4 over x in [0, 6] with an ogive (tangent
-    circular-arc) nose over the first 1.2, fixed. Wing: the config-0 wing
-    scaled x3 (semi-span 3, root chord 3 at the fuselage side y = 0.4... the
-    planform is the config-0 one scaled to semi-span 3, rooted at y = 0.4),
-    root leading edge at x = 2. Pylon: a flat plate under the wing at
-    y = 1.2. Nacelle: cylindrical shell r = 0.15, length 0.8 below the pylon.
-    Pylon and nacelle move rigidly with the wing section at y = 1.2.
+    circular-arc) nose over the first 1.2, fixed (zero displacement).
+    Wing: the config-0 wing scaled uniformly by 3 (semi-span 3, chord
+    3.0 -> 1.5, 25 deg sweep, NACA0012), leading edge at x = 2 on the
+    centre line; only its exposed part, y in [0.4, 3] (outboard of the
+    fuselage radius), carries points. Pylon: a flat plate of height 0.25 at
+    y = 1.2, hung below the wing's thickest point (z <= -0.15). Nacelle:
+    cylindrical shell r = 0.15, length 0.8, below the pylon. Pylon and
+    nacelle move rigidly with the wing section at y = 1.2.
     """
     rng = np.random.default_rng(seed)
     b = 3.0
-    geom = WingGeometry(semi_span=b, root_chord=1.5, tip_chord=0.75, y0=0.4)
+    geom = WingGeometry(semi_span=b, root_chord=3.0, tip_chord=1.5)
+    y_root = 0.4  # fuselage radius: the wing is exposed over y in [0.4, 3]
     x_root = 2.0
     r_f, l_f, l_nose = 0.4, 6.0, 1.2
     y_p, r_n, l_n = 1.2, 0.15, 0.8
 
     # component areas (approximate, for the point split)
     a_fus = 2 * np.pi * r_f * (l_f - l_nose) + np.pi * r_f * np.hypot(r_f, l_nose)
-    span_w = b - geom.y0
-    a_wing = 2.04 * 0.5 * (geom.root_chord + geom.tip_chord) * span_w
+    span_w = b - y_root
+    a_wing = 2.04 * 0.5 * (geom.chord(y_root) + geom.tip_chord) * span_w
     c_p = geom.chord(y_p)
     h_p = 0.25
+    z_p = 0.15  # below the wing's half-thickness at y_p (0.06 * chord = 0.144)
     a_pyl = 2 * 0.6 * c_p * h_p
     a_nac = 2 * np.pi * r_n * l_n
     areas = np.array([a_fus, a_wing, a_pyl, a_nac])
@@ -213,7 +217,7 @@ def wing_body(nb=200_000, nv=40_000_000, seed=0, m=64, radius=4.0, tol_frac=1e-4
         return np.column_stack([x, r * np.cos(ang), r * np.sin(ang)])
 
     def wing(n):
-        y = rng.uniform(geom.y0, b, n)
+        y = rng.uniform(y_root, b, n)
         s = rng.uniform(0.0, 1.0, n)
         xi, zc = _arc().at(s)
         p = geom.surface(y, xi, zc)
@@ -224,14 +228,14 @@ def wing_body(nb=200_000, nv=40_000_000, seed=0, m=64, radius=4.0, tol_frac=1e-4
 
     def pylon(n):
         xs = x_le_p + c_p * rng.uniform(0.2, 0.8, n)
-        zs = -rng.uniform(0.0, h_p, n) - 0.01
+        zs = -rng.uniform(0.0, h_p, n) - z_p
         side = np.where(rng.uniform(size=n) < 0.5, -0.005, 0.005)
         return np.column_stack([xs, y_p + side, zs])
 
     def nacelle(n):
         xs = x_le_p - 0.3 + rng.uniform(0.0, l_n, n)
         ang = rng.uniform(0.0, 2 * np.pi, n)
-        zc = -h_p - r_n - 0.02
+        zc = -z_p - h_p - r_n - 0.02
         return np.column_stack([xs, y_p + r_n * np.cos(ang), zc + r_n * np.sin(ang)])
 
     parts = [fuselage(counts[0]), wing(counts[1]), pylon(counts[2]), nacelle(counts[3])]

@@ -37,6 +37,16 @@ def load_golden(name):
         return {k: z[k] for k in z.files}
 
 
+def digest(*arrays):
+    """SHA-256 of the arrays' bytes (tests/golden/make_golden.py's generator check)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
 def reference_available():
     return (REFERENCE_SRC / "rbfdeform" / "core.py").exists()
 

@@ -10,8 +10,10 @@ Tolerances (floating point, FP64 throughout):
   * weights: norm-wise max|dW| / max|W| <= 1e-9 where kappa(Phi) <= 1e8
     (configs 0/1, small cases). At kappa ~ 4e9 (config-2 style grid) two
     backward-stable solves of the same system already differ by ~2e-9
-    norm-wise, so the bar there is 2e-8; at kappa = 2.4e10
-    (config 3, R = 4) they differ by 3e-8 and the bar is 1e-7.
+    norm-wise, so the bar there is 2e-8. For the large goldens
+    (configs[3] at full size, configs[4]) the golden records the reference's
+    own spread (a second stable solve of the same system) and the bars are
+    4 x that spread, floored at 1e-9.
 """
 
 import numpy as np
@@ -236,17 +238,29 @@ def test_solve_support_weights_recovers(cuda, rng):
 
 
 # --------------------------------------------------------------- selection
+# (golden, weight tolerance). Goldens made by tests/golden/make_golden_large.py also
+# carry the reference's OWN spread at their conditioning: the same support set solved
+# a second backward-stable way (one blocked Cholesky of the assembled Phi) moves the
+# weights by alt_w_rel and the displacements by alt_u_rel. For those the bars are
+# max(1e-9, 4 x spread) (None below): no solver can be held closer to the reference
+# than the reference is to itself. Observed deviations are written to
+# gpurun_out/parity_deviations.json.
 GOLDEN_SELECTIONS = [
     ("hemisphere_m1", 1e-9), ("hemisphere_m4", 1e-9), ("smooth0_m1", 1e-9), ("smooth0_m5", 1e-9),
     ("smooth3_m1", 1e-9), ("smooth3_m5", 1e-9), ("smooth11_m1", 1e-9), ("smooth11_m5", 1e-9),
     ("cfg0_m1", 1e-9), ("cfg0_m8", 1e-9), ("cfg1_m32", 1e-9), ("cfg2s_m48", 2e-8),
     ("switch_m8", 1e-9),  # n = 1200: crosses from the shared-memory path to the L2 path
     ("cfg2_m48", 2e-8),   # BASELINE configs[2] at full size (Nb = 80k): MSG -> GRID hand-over
-    # configs[3] at full size (Nb = 200k, GRID path), first 400 supports: R = 4 makes Phi
-    # very ill-conditioned (kappa = 2.4e10, |w| up to 1.8e5); two stable solves of the same
-    # system differ by 3e-8 norm-wise (displacements 1.5e-8), so the bar is 1e-7
+    # configs[3] at full size (Nb = 200k, R = 4, GRID path): first 400 supports (also
+    # pinned oracle-vs-reference bitwise), then the whole run (4,872 supports)
     ("cfg3_m64_cap400", 1e-7),
+    ("cfg3_m64", None),
+    # configs[4] on the configs[2] wing: greedy (m = 1), m = Nb/Nc, 1.5 Nb/Nc, 2 Nb/Nc,
+    # and the global-support stress (R = bounding-box diagonal, m = 141, cap 1500)
+    ("cfg4_m1", None), ("cfg4_m94", None), ("cfg4_m141", None), ("cfg4_m187", None),
+    ("cfg4_stress", None),
 ]
+_DEVIATIONS = {}
 
 
 def golden_inputs(name, g):
@@ -256,7 +270,7 @@ def golden_inputs(name, g):
         wl = W.config(0, nv=100_000)
     elif name.startswith("cfg1"):
         wl = W.config(1, nv=2_000_000)
-    elif name == "cfg2_m48":
+    elif name == "cfg2_m48" or name.startswith("cfg4"):
         wl = W.config(2, nv=200_000)
     elif name.startswith("cfg3"):
         wl = W.config(3, nv=100_000)
@@ -265,41 +279,77 @@ def golden_inputs(name, g):
     return wl.points, wl.disp, wl
 
 
+def _record_deviation(name, **vals):
+    import json
+    from pathlib import Path
+
+    _DEVIATIONS[name] = vals
+    print(name, vals)
+    out = Path(__file__).resolve().parent.parent / "gpurun_out"
+    if out.is_dir():
+        (out / "parity_deviations.json").write_text(json.dumps(_DEVIATIONS, indent=1))
+
+
 @pytest.mark.parametrize("name,wtol", GOLDEN_SELECTIONS)
 def test_selection_matches_reference_golden(cuda, name, wtol):
     g = load_golden(name)
     pts, disp, wl = golden_inputs(name, g)
+    if "digest" in g and wl is not None and name.startswith(("cfg3", "cfg4")):
+        from conftest import digest
+
+        assert digest(pts, disp) == str(g["digest"]), "generator drift: regenerate the golden"
     radius, tol, cap, m, seed = g["params"]
+    if wtol is None:  # bars from the reference's own spread (make_golden_large.py)
+        wtol = max(1e-9, 4 * float(g["alt_w_rel"]))
+        utol = max(1e-9, 4 * float(g["alt_u_rel"]))
+    else:
+        utol = 1e-9 if wtol <= 2e-8 else 1e-7
     b = cuda.BoundarySet(np.arange(len(pts)), pts, disp)
     cfg = cuda.SelectionConfig(radius=radius, tol=tol, max_supports=int(cap), m=int(m), seed=int(seed))
     res = cuda.gcb_select(b, cfg)
-    assert np.array_equal(res.support.nodes, g["seq"]), "support-node sequence differs"
     recs = res.history.records
+    lm = np.array([r.local_max_error for r in recs])
+    seq = np.asarray(res.support.nodes)
+    same = len(seq) == len(g["seq"]) and bool(np.array_equal(seq, g["seq"]))
+    first_diff = None if same else int(np.flatnonzero(
+        np.append(seq[: len(g["seq"])] != g["seq"][: len(seq)], True))[0])
+    dev = {"nc": int(len(seq)), "nc_ref": int(len(g["seq"])), "sequence_identical": same,
+           "first_difference": first_diff, "w_tol": wtol, "u_tol": utol}
+    if same:
+        dev["w_rel"] = rel(res.support.weights, g["weights"])
+        if len(lm) == len(g["rec_local_max"]):
+            dev["local_max_rel"] = float(np.abs(lm - g["rec_local_max"]).max() / g["rec_local_max"].max())
+        dev["final_max_rel"] = abs(res.history.final_sweep.local_max_error - float(g["final_max"])) / max(
+            float(g["final_max"]), 1e-300)
+        if wl is not None:
+            u = cuda.evaluate_displacements(wl.volume[g["vol_idx"]], res.support, radius)
+            dev["u_rel"] = rel(u, g["vol_u"])
+        if "alt_w_rel" in g:
+            dev["ref_spread_w"] = float(g["alt_w_rel"])
+            dev["ref_spread_u"] = float(g["alt_u_rel"])
+    _record_deviation(name, **dev)
+    assert same, f"support-node sequence differs from position {first_diff}"
     assert [r.iteration for r in recs] == g["rec_iter"].tolist()
     assert [r.group for r in recs] == g["rec_group"].tolist()
     assert [r.node for r in recs] == g["rec_node"].tolist()
     assert [r.kernel_evals for r in recs] == g["rec_evals"].tolist()
     assert [r.cum_kernel_evals for r in recs] == g["rec_cum"].tolist()
-    lm = np.array([r.local_max_error for r in recs])
-    # per-record maxima: 1e-9 relative; 1e-8 at kappa ~ 4e9; at configs[3]'s
-    # kappa = 2.4e10 the inherent spread of the residuals is ~1.5e-8
-    lm_tol = 1e-9 if wtol <= 1e-9 else (1e-8 if wtol <= 2e-8 else 3e-8)
-    assert np.abs(lm - g["rec_local_max"]).max() <= lm_tol * g["rec_local_max"].max()
+    # per-record maxima and the final sweep: 1e-9 relative (to the largest record)
+    # where the weights are held to 1e-9; otherwise the displacement bar
+    lm_tol = 1e-9 if wtol <= 1e-9 else max(1e-8, utol)
+    assert dev["local_max_rel"] <= lm_tol
     f = res.history.final_sweep
     assert [f.iteration, f.node, f.kernel_evals, f.cum_kernel_evals] == g["final"].tolist()
     assert f.group == -1
-    # the final sweep's residuals cancel against |w| up to 1.8e5 at configs[3]'s
-    # kappa = 2.4e10: summation-order rounding there is ~1e-7 relative
-    f_tol = 1e-7 if wtol <= 2e-8 else 1e-6
+    # the final maximum is a residual (|d - u| ~ tol): its relative rounding is the
+    # displacement deviation scaled by max|d| / tol
+    f_tol = 1e-9 if wtol <= 1e-9 else max(1e-7, utol * float(np.abs(disp).max()) / tol)
     assert f.local_max_error == pytest.approx(float(g["final_max"]), rel=f_tol, abs=1e-16)
     assert res.converged == bool(g["converged"])
-    assert rel(res.support.weights, g["weights"]) <= wtol
+    assert dev["w_rel"] <= wtol
     assert np.array_equal(res.support.points, pts[g["seq"]])
     if wl is not None:
-        u = cuda.evaluate_displacements(wl.volume[g["vol_idx"]], res.support, radius)
-        # displacements: 1e-9 (north_star); at kappa = 2.4e10 (configs[3], R = 4) an
-        # alternative stable solve of the reference's own system moves them by 1.5e-8
-        assert rel(u, g["vol_u"]) <= (1e-9 if wtol <= 2e-8 else 1e-7)
+        assert dev["u_rel"] <= utol
 
 
 def test_selection_determinism_and_greedy_alias(cuda):

@@ -156,3 +156,17 @@ def test_oracle_metrics_match_reference_golden():
     assert [h[0] for _, h in hist] == g["hist_max"].tolist()
     assert [h[1] for _, h in hist] == g["hist_rms"].tolist()
     assert [h[2] for _, h in hist] == g["hist_node"].tolist()
+
+
+@pytest.mark.parametrize("name", ["cfg3_m64", "cfg4_m1", "cfg4_m94", "cfg4_m141", "cfg4_m187", "cfg4_stress"])
+def test_large_goldens_match_generator(name):
+    """The large reference runs (tests/golden/make_golden_large.py) were made on
+    the current workload generators: same boundary bits, and the recorded
+    second-solve spread is present."""
+    from conftest import digest
+
+    g = load_golden(name)
+    wl = W.config(3, nv=10) if name.startswith("cfg3") else W.config(2, nv=10)
+    assert digest(wl.points, wl.disp) == str(g["digest"])
+    assert float(g["alt_u_rel"]) < 1e-7 and len(g["seq"]) == len(g["weights"])
+    assert int(g["params"][2]) == (1500 if name == "cfg4_stress" else wl.nb)
