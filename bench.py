@@ -328,6 +328,10 @@ def run_ours(args, rank, world, local):
     from paper_2004_04817_b200 import _native as N
     from paper_2004_04817_b200 import multi
 
+    # RBF_BENCH_SHARE_GPU=1 (code-path check on a one-GPU box, with RBF_BENCH_BACKEND=gloo:
+    # no kernel waits on another rank): every rank on device 0; numbers are not a measurement
+    if os.environ.get("RBF_BENCH_SHARE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group(os.environ.get("RBF_BENCH_BACKEND", "nccl"),
