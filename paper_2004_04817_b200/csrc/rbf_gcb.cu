@@ -47,7 +47,8 @@ static_assert(kLoopThreads == 512, "scan prologues shift by log2(kLoopThreads) =
 constexpr int kClusterCTAs = 16;
 static_assert(kClusterCTAs == 16, "one-cluster scans split rows with >> 4");
 constexpr int kSupTile = 2048;       // GlobalPath: supports staged per scan tile
-constexpr int kRowSmemMax = 8192;    // GlobalPath: row held in shared memory
+constexpr int kRowSmemMax = 8192;    // GlobalPath: row held in shared memory below this n
+                                     // (beyond it, in global scratch: LoopScratch::rowg)
 constexpr int kSmallMax = 1024;      // SmemPath: supports resident in shared memory
 constexpr int kAutoClusterMaxCard = 2048;
 constexpr int64_t kClusterScanPairs = 400000;  // per group scan, see gcb_driver
@@ -83,6 +84,8 @@ struct LoopScratch {
   double* xc;      // [2 parities][16 clusters][4]: per-cluster (err, pos) x 2
   unsigned* xseq;  // [2][16] publication sequence numbers
   double* lic;     // [cap(cap+1)/2] column-packed copy of Li (L2 paths)
+  double* rowg;    // [ctas][cap] candidate rows once n >= kRowSmemMax (L2 paths; one per
+                   // CTA: every CTA computes the whole row, as in shared memory below it)
 };
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
@@ -111,6 +114,7 @@ static LoopScratch carve(void* base, int nb, int cap, int ctas, size_t* total) {
   s.xc = reinterpret_cast<double*>(take(sizeof(double) * 2 * 16 * 4));
   s.xseq = reinterpret_cast<unsigned*>(take(sizeof(unsigned) * 2 * 16));
   s.lic = reinterpret_cast<double*>(take(sizeof(double) * (size_t)cap * (cap + 1) / 2));
+  s.rowg = reinterpret_cast<double*>(take(cap >= kRowSmemMax ? sizeof(double) * (size_t)ctas * cap : 8));
   if (total) *total = off;
   return s;
 }
@@ -278,7 +282,7 @@ struct GlobalPath {
   double inv_r;
   Clock& pc;
 
-  static constexpr int kMaxN = kRowSmemMax;
+  static constexpr int kMaxN = 1 << 30;  // the factor grows with the capacity (host side)
   __device__ Common& cm() { return sh.cm; }
   __device__ void sync() { team.sync(); }
   // rebuild the column-packed copy of Li (rows < n) for this launch's capacity
@@ -553,7 +557,7 @@ struct GlobalPath {
   // x (n doubles) into shared memory (the scan's staging area is idle
   // during an append) once it is long enough for the copy to pay
   __device__ __forceinline__ const double* stage_x(const double* x, int n) {
-    if (n <= 1024) return nullptr;
+    if (n <= 1024 || n > kRowSmemMax) return nullptr;
     double* xs = sh.sx;  // sx..wz: 6 * kSupTile contiguous doubles >= kRowSmemMax
     for (int j = threadIdx.x; j < n; j += kLoopThreads) xs[j] = __ldcg(x + j);
     __syncthreads();
@@ -566,7 +570,7 @@ struct GlobalPath {
     const int cap = a.cap;
     const double px = __ldg(a.points + 3 * (int64_t)pos), py = __ldg(a.points + 3 * (int64_t)pos + 1),
                  pz = __ldg(a.points + 3 * (int64_t)pos + 2);
-    double* row = sh.row;
+    double* row = n < kRowSmemMax ? sh.row : s.rowg + (int64_t)blockIdx.x * cap;
     const bool near = exact_row(sh.cm, row, n, px, py, pz, a.radius, a.dup_dist, [&](int j, double& x, double& y, double& z) {
       x = __ldcg(a.sup + j);
       y = __ldcg(a.sup + cap + j);
@@ -2689,12 +2693,14 @@ extern "C" int rbf_gcb_run(const rbf_gcb_args* args, void* stream) {
       const int max_cl = sm_count(dev) / kClusterCTAs;
       ncl = a.clusters > 0 ? a.clusters : kMsgDefaultClusters;
       ncl = ncl < 1 ? 1 : (ncl > max_cl ? max_cl : (ncl > 16 ? 16 : ncl));
-      RBF_CUDA_TRY(cudaMemsetAsync(s.xseq, 0, sizeof(unsigned) * 2 * 16, st));
     }
     if (tail) acopy.flags |= kFlagTailSweep;
     for (int r = 0; r < rounds; ++r) {
       rbf_gcb_args x = acopy;
       if (r > 0) x.flags |= kFlagResumeOnly;
+      // every MSG launch counts its cross-cluster publications from 0
+      // (MsgPath::gathers): clear the sequence words before each one
+      if (mode == RBF_GCB_MSG) RBF_CUDA_TRY(cudaMemsetAsync(s.xseq, 0, sizeof(unsigned) * 2 * 16, st));
       if (mode == RBF_GCB_MSG)
         RBF_CUDA_TRY(launch_cluster(ph ? (const void*)gcb_msg_kernel<true> : (const void*)gcb_msg_kernel<false>,
                                     x, s, sizeof(MsgShared), st, ncl));

@@ -490,7 +490,6 @@ def _read_state(buf):
     return N.GcbState.from_buffer_copy(raw)
 
 
-_DEVICE_MAX_SUPPORTS = 8192  # kRowSmemMax in csrc/rbf_gcb.cu
 
 
 def _initial_capacity(config, nb):
@@ -596,11 +595,8 @@ def _gcb_run(boundary, config, mode=None, phases=None, sweep=True):
             args.mode = resolved.value
             buf.resize_scratch(ctas.value)
             continue
-        if st.n >= _DEVICE_MAX_SUPPORTS - 1:
-            raise N.NativeUnavailableError(
-                f"support count exceeds the device loop limit ({_DEVICE_MAX_SUPPORTS - 1})")
         if st.n >= buf.cap:
-            buf._grow_factor(max(min(2 * buf.cap, limit, _DEVICE_MAX_SUPPORTS), st.n + 1), st.n)
+            buf._grow_factor(max(min(2 * buf.cap, limit), st.n + 1), st.n)
         if st.n_records >= buf.rec_cap:
             buf._grow_records(2 * buf.rec_cap, st.n_records)
 

@@ -7,6 +7,10 @@ Companion to make_golden.py (same output schema, same ``run_selection``):
                       inverse-factor parity at kappa >= 1e10.
 * ``cfg4_m1``         configs[4]: the original greedy (m = 1) on the configs[2] wing.
 * ``cfg4_m<k>``       configs[4]: m = round(f * Nb / Nc), f in {1, 1.5, 2}, Nc from cfg4_m1.
+* ``bign_m``          more than 8,192 supports (past the round-1 device limit): 9,000
+                      random nodes in the unit cube, R = 0.15 (well conditioned),
+                      m = Nb (single-node groups: every visit appends), cap 8,500 --
+                      the loop runs MSG -> SMEM -> GRID and crosses n = 8,192.
 * ``cfg4_stress``     configs[4] global-support stress: R = bounding-box diagonal of the
                       boundary and (a strided 1M sample of) the volume, m = the 1.5 Nb/Nc
                       entry, support cap 1500 (tools/msweep.py's stress).
@@ -132,6 +136,17 @@ def case_cfg4():
         return
     sp, u = alt_solve(wl.points, wl.disp, res, diag, wl.volume[idx])
     MG.save("cfg4_stress", digest=dig, vol_idx=idx, vol_u=u, **out, **sp)
+
+
+def case_bign():
+    rng = np.random.default_rng(8192)
+    pts = rng.uniform(0.0, 1.0, (9000, 3))
+    disp = np.stack([0.02 * np.sin(3 * pts[:, 0] + 1), 0.02 * np.cos(2 * pts[:, 1]),
+                     0.02 * np.sin(4 * pts[:, 2] + pts[:, 0])], 1)
+    out, res = run(pts, disp, 0.15, 1e-300, 8500, len(pts))
+    q = rng.uniform(0.0, 1.0, (4096, 3))
+    u = R.evaluate_displacements(q, res.support, 0.15, workers=WORKERS)
+    MG.save("bign_m", points=pts, disp=disp, targets=q, vol_u=u, **out)
 
 
 if __name__ == "__main__":
