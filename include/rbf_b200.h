@@ -258,7 +258,9 @@ typedef struct rbf_gcb_args {
   double* L;                /* packed, cap*(cap+1)/2 */
   double* Li;               /* packed, cap*(cap+1)/2 */
   double* y;                /* (cap, 3) forward-substituted displacements */
-  double* sup;              /* (6, cap) SoA: x, y, z, wx, wy, wz           */
+  double* sup;              /* (12, cap) SoA: x, y, z, wx, wy, wz (weights), then the
+                               compensated weights' hi (3 rows) and lo (3 rows): the
+                               loop carries each weight as hi + lo */
   int32_t* sel;             /* (cap) selected positions in order          */
   uint8_t* inel;            /* (nb) ineligible flags                       */
   int32_t cap;

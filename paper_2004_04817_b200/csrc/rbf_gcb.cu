@@ -260,6 +260,24 @@ __device__ __forceinline__ bool exact_row(Common& cm, double* row, int n, double
   return cm.dbl[0] != 0.0;
 }
 
+// Compensated incremental weights. Every append moves the
+// weights by Li[n][j] y_n; summed naively over thousands of appends the
+// rounding of those updates drifts the residuals by more than the gap between
+// near-tied candidates at kappa ~ 1e10 (configs[3]: the sequence left the
+// reference's at support 4,125). So each weight is carried as hi + lo: the
+// product's rounding error (an FMA) and the sum's (two-sum) accumulate in lo,
+// and the scans read the rounded hi + lo.
+__device__ __forceinline__ double comp_add(double& hi, double& lo, double a, double b) {
+  const double p = __dmul_rn(a, b);
+  const double pe = fma(a, b, -p);
+  const double t = __dadd_rn(hi, p);
+  const double bb = __dsub_rn(t, hi);
+  const double e = __dadd_rn(__dsub_rn(hi, __dsub_rn(t, bb)), __dsub_rn(p, bb));
+  hi = t;
+  lo = __dadd_rn(lo, __dadd_rn(e, pe));
+  return __dadd_rn(hi, lo);
+}
+
 // ================================================================ GlobalPath
 // column j of a column-packed lower triangle with capacity cap: entries
 // i = j .. cap-1 contiguous from here
@@ -285,6 +303,10 @@ struct GlobalPath {
   static constexpr int kMaxN = 1 << 30;  // the factor grows with the capacity (host side)
   __device__ Common& cm() { return sh.cm; }
   __device__ void sync() { team.sync(); }
+  // shared-memory (err, pos) cache for the tail launch's walk over group
+  // bests: the scan staging area (sx..wz), idle once a scan has been gathered
+  __device__ Best* best_cache() { return reinterpret_cast<Best*>(sh.sx); }
+  __device__ static constexpr int best_cache_cap() { return (int)(6 * kSupTile * sizeof(double) / sizeof(Best)); }
   // rebuild the column-packed copy of Li (rows < n) for this launch's capacity
   __device__ void begin(int n) {
     const int64_t total = (int64_t)n * (n + 1) / 2;
@@ -498,7 +520,7 @@ struct GlobalPath {
   // column-packed copy (vector j = rows j..n-1, x index j + e); one warp per
   // vector, vectors strided over every warp of the team, 16 loads per lane
   // in flight once the factor is long. finish(v, sum) runs on lane 0.
-  // pre(v) -> double4: the finishing lane's operands of vector v, loaded
+  // pre(v) -> POD: the finishing lane's operands of vector v, loaded
   // before the dot product so their L2 latency overlaps it
   template <bool kCols, class XL, class Pre, class Fin>
   __device__ __forceinline__ void tri_gemv(const double* A, int n, XL xload, Pre pre, Fin finish) {
@@ -515,7 +537,8 @@ struct GlobalPath {
       const int warp = threadIdx.x >> 5, grp = warp / wpr, sub = warp % wpr;
       const int v = grp * G + (int)blockIdx.x;  // rows interleaved over the CTAs
       double acc = 0.0;
-      const double4 pf = (v < n && sub == 0 && lane == 0) ? pre(v) : make_double4(0.0, 0.0, 0.0, 0.0);
+      decltype(pre(0)) pf{};
+      if (v < n && sub == 0 && lane == 0) pf = pre(v);
       if (v < n) {
         const double* av = A + (kCols ? col_off(v, cap) : tri_off(v));
         const int len = kCols ? n - v : v + 1;
@@ -548,7 +571,8 @@ struct GlobalPath {
       const double* av = A + (kCols ? col_off(v, cap) : tri_off(v));
       const int len = kCols ? n - v : v + 1;
       auto xl = [&](int e) { return xload(v, e); };
-      const double4 pf = lane == 0 ? pre(v) : make_double4(0.0, 0.0, 0.0, 0.0);
+      decltype(pre(0)) pf{};
+      if (lane == 0) pf = pre(v);
       const double acc = len > 1024 ? row_dot<16>(av, len, xl, lane) : row_dot<8>(av, len, xl, lane);
       if (lane == 0) finish(v, acc, pf);
     }
@@ -654,20 +678,36 @@ struct GlobalPath {
     // move by Li[n][j] y_n (w = Li^T y with the new row appended)
     const int nn = n;
     xs = stage_x(s.c1, n);
+    double* whi = a.sup + 6 * (int64_t)cap;  // compensated weights: hi (3 rows), lo (3 rows)
+    double* wlo = a.sup + 9 * (int64_t)cap;
+    struct Pf7 {
+      double c, h[3], l[3];
+    };
     tri_gemv<true>(
         s.lic, n, [&](int v, int e) { return xs ? xs[v + e] : __ldcg(s.c1 + v + e); },
         [&](int j) {
-          return make_double4(__ldcg(s.c1 + j), __ldcg(wgt + j), __ldcg(wgt + cap + j),
-                              __ldcg(wgt + 2 * cap + j));
+          Pf7 q;
+          q.c = __ldcg(s.c1 + j);
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            q.h[k] = __ldcg(whi + k * (int64_t)cap + j);
+            q.l[k] = __ldcg(wlo + k * (int64_t)cap + j);
+          }
+          return q;
         },
-        [&](int j, double u, const double4& pf) {
+        [&](int j, double u, const Pf7& pf) {
           const double lij = -u * inv_l;
           Lirow[j] = lij;
           s.lic[col_off(j, cap) + (nn - j)] = lij;
-          Lrow[j] = pf.x;
-          wgt[j] = fma(lij, yn0, pf.y);
-          wgt[cap + j] = fma(lij, yn1, pf.z);
-          wgt[2 * cap + j] = fma(lij, yn2, pf.w);
+          Lrow[j] = pf.c;
+          const double yn[3] = {yn0, yn1, yn2};
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            double h = pf.h[k], lo = pf.l[k];
+            wgt[k * (int64_t)cap + j] = comp_add(h, lo, lij, yn[k]);
+            whi[k * (int64_t)cap + j] = h;
+            wlo[k * (int64_t)cap + j] = lo;
+          }
         });
     if (blockIdx.x == 0 && tid == 0) {
       Lirow[n] = inv_l;
@@ -679,9 +719,10 @@ struct GlobalPath {
       a.sup[n] = px;
       a.sup[cap + n] = py;
       a.sup[2 * cap + n] = pz;
-      wgt[n] = yn0 * inv_l;
-      wgt[cap + n] = yn1 * inv_l;
-      wgt[2 * cap + n] = yn2 * inv_l;
+      wgt[n] = whi[n] = yn0 * inv_l;
+      wgt[cap + n] = whi[cap + n] = yn1 * inv_l;
+      wgt[2 * cap + n] = whi[2 * cap + n] = yn2 * inv_l;
+      wlo[n] = wlo[cap + n] = wlo[2 * cap + n] = 0.0;
       a.sel[n] = pos;
     }
     if (tid == 0) a.inel[pos] = 1;
@@ -804,6 +845,8 @@ struct SmemPath {
   Clock& pc;
 
   static constexpr int kMaxN = kSmallMax;
+  __device__ Best* best_cache() { return nullptr; }  // (the tail launch is a GlobalPath)
+  __device__ static constexpr int best_cache_cap() { return 0; }
   static constexpr int kTPT = 4;  // targets per lane in group scans
   __device__ Common& cm() { return sh.cm; }
   __device__ void sync() { cg::this_cluster().sync(); }
@@ -1136,11 +1179,12 @@ struct SmemPath {
       *at(&sh.wx[j], q) = w0;
       *at(&sh.wy[j], q) = w1;
       *at(&sh.wz[j], q) = w2;
-      if (q == 0) {
+      if (q == 0) {  // fresh weights (Li^T y): hi = w, lo = 0 for the compensated paths
         Lirow[j] = lij;
-        wgt[j] = w0;
-        wgt[cap + j] = w1;
-        wgt[2 * cap + j] = w2;
+        wgt[j] = wgt[3 * cap + j] = w0;  // (wgt = sup row 3: rows 6-8 hi, 9-11 lo)
+        wgt[cap + j] = wgt[4 * cap + j] = w1;
+        wgt[2 * cap + j] = wgt[5 * cap + j] = w2;
+        wgt[6 * cap + j] = wgt[7 * cap + j] = wgt[8 * cap + j] = 0.0;
       }
     }
     if (tid == 0) {  // the new support, in every CTA's resident copy
@@ -1166,9 +1210,10 @@ struct SmemPath {
         a.sup[n] = px;
         a.sup[cap + n] = py;
         a.sup[2 * cap + n] = pz;
-        wgt[n] = yn0 * inv_l;
-        wgt[cap + n] = yn1 * inv_l;
-        wgt[2 * cap + n] = yn2 * inv_l;
+        wgt[n] = wgt[3 * cap + n] = yn0 * inv_l;
+        wgt[cap + n] = wgt[4 * cap + n] = yn1 * inv_l;
+        wgt[2 * cap + n] = wgt[5 * cap + n] = yn2 * inv_l;
+        wgt[6 * cap + n] = wgt[7 * cap + n] = wgt[8 * cap + n] = 0.0;
         a.sel[n] = pos;
       }
     }
@@ -1225,7 +1270,8 @@ struct MsgShared {
   Common cm;
   double ux[kMsgMax], uy[kMsgMax], uz[kMsgMax];  // support coordinates
   double sx[kMsgMax], sy[kMsgMax], sz[kMsgMax];  // ... scaled by 1/R
-  double wx[kMsgMax], wy[kMsgMax], wz[kMsgMax];  // weights
+  double wx[kMsgMax], wy[kMsgMax], wz[kMsgMax];  // weights (hi + lo, what the scans read)
+  double wh[3][kMsgMax], wl[3][kMsgMax];         // compensated weights: hi, lo (comp_add)
   double y0[kMsgMax], y1[kMsgMax], y2[kMsgMax];  // forward-substituted d
   double row[kMsgMax], c0[kMsgMax], r[kMsgMax], c1[kMsgMax];
   double Lown[kMsgOwnElems], Liown[kMsgOwnElems];  // owned rows i = 16 q + rank
@@ -1281,6 +1327,8 @@ struct MsgPath {
   unsigned phase_bits;  // parity of the next completion of each mbarrier
 
   static constexpr int kMaxN = kMsgMax;
+  __device__ Best* best_cache() { return nullptr; }  // (the tail launch is a GlobalPath)
+  __device__ static constexpr int best_cache_cap() { return 0; }
   __device__ Common& cm() { return sh.cm; }
   unsigned gathers;  // publications so far (cross-cluster sequence numbers)
   __device__ int rank() const { return blockIdx.x % kClusterCTAs; }
@@ -1359,6 +1407,11 @@ struct MsgPath {
       sh.wx[j] = __ldcg(a.sup + 3 * cap + j);
       sh.wy[j] = __ldcg(a.sup + 4 * cap + j);
       sh.wz[j] = __ldcg(a.sup + 5 * cap + j);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        sh.wh[k][j] = __ldcg(a.sup + (6 + k) * (int64_t)cap + j);
+        sh.wl[k][j] = __ldcg(a.sup + (9 + k) * (int64_t)cap + j);
+      }
       sh.y0[j] = __ldcg(a.y + 3 * j);
       sh.y1[j] = __ldcg(a.y + 3 * j + 1);
       sh.y2[j] = __ldcg(a.y + 3 * j + 2);
@@ -2066,9 +2119,10 @@ struct MsgPath {
         a.sup[n] = px;
         a.sup[cap + n] = py;
         a.sup[2 * cap + n] = pz;
-        wgt[n] = yn0 * inv_l;
-        wgt[cap + n] = yn1 * inv_l;
-        wgt[2 * cap + n] = yn2 * inv_l;
+        wgt[n] = wgt[3 * cap + n] = yn0 * inv_l;  // (wgt = sup row 3: rows 6-8 hi, 9-11 lo)
+        wgt[cap + n] = wgt[4 * cap + n] = yn1 * inv_l;
+        wgt[2 * cap + n] = wgt[5 * cap + n] = yn2 * inv_l;
+        wgt[6 * cap + n] = wgt[7 * cap + n] = wgt[8 * cap + n] = 0.0;
         a.sel[n] = pos;
         Lirow_g[n] = inv_l;
         a.L[tri_off(n) + n] = l;
@@ -2088,23 +2142,38 @@ struct MsgPath {
     }
     wait(kMbW);
     if (kOv) bar_ov();  // the next group's scan has read the old weights
-    for (int j = tid; j < n; j += kTA) {  // x' = x + Li[n][j] y_n
+    for (int j = tid; j < n; j += kTA) {  // x' = x + Li[n][j] y_n, compensated (comp_add)
       const double lij = sh.u_all[j] * neg_inv_l;
-      sh.wx[j] = fma(lij, yn0, sh.wx[j]);
-      sh.wy[j] = fma(lij, yn1, sh.wy[j]);
-      sh.wz[j] = fma(lij, yn2, sh.wz[j]);
+      double h0 = sh.wh[0][j], l0 = sh.wl[0][j], h1 = sh.wh[1][j], l1 = sh.wl[1][j];
+      double h2 = sh.wh[2][j], l2 = sh.wl[2][j];
+      sh.wx[j] = comp_add(h0, l0, lij, yn0);
+      sh.wy[j] = comp_add(h1, l1, lij, yn1);
+      sh.wz[j] = comp_add(h2, l2, lij, yn2);
+      sh.wh[0][j] = h0;
+      sh.wl[0][j] = l0;
+      sh.wh[1][j] = h1;
+      sh.wl[1][j] = l1;
+      sh.wh[2][j] = h2;
+      sh.wl[2][j] = l2;
       if (rk == owner) sh.Liown[own_off(qn, owner) + j] = lij;
       if (j % kClusterCTAs == rk && cluster() == 0) {  // my columns -> global copies
         wgt[j] = sh.wx[j];
         wgt[cap + j] = sh.wy[j];
         wgt[2 * cap + j] = sh.wz[j];
+        wgt[3 * cap + j] = h0;
+        wgt[4 * cap + j] = h1;
+        wgt[5 * cap + j] = h2;
+        wgt[6 * cap + j] = l0;
+        wgt[7 * cap + j] = l1;
+        wgt[8 * cap + j] = l2;
         Lirow_g[j] = lij;
       }
     }
     if (tid == 0) {
-      sh.wx[n] = yn0 * inv_l;
-      sh.wy[n] = yn1 * inv_l;
-      sh.wz[n] = yn2 * inv_l;
+      sh.wx[n] = sh.wh[0][n] = yn0 * inv_l;
+      sh.wy[n] = sh.wh[1][n] = yn1 * inv_l;
+      sh.wz[n] = sh.wh[2][n] = yn2 * inv_l;
+      sh.wl[0][n] = sh.wl[1][n] = sh.wl[2][n] = 0.0;
     }
     n += 1;
     sync_a<kOv>();
@@ -2292,6 +2361,13 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
       __syncthreads();
     }
     P.sync();
+    // the walk below visits the groups one after another: their bests come
+    // from shared memory, not one dependent L2 load per group (~40 % of the
+    // launch, profiles/r02_ncu_summary.md)
+    Best* gcache = P.best_cache();
+    const int ncache = m < P.best_cache_cap() ? m : P.best_cache_cap();
+    for (int g = tid; g < ncache; g += kLoopThreads) gcache[g] = Best{__ldcg(&gbest[g].err), __ldcg(&gbest[g].pos)};
+    __syncthreads();
     const uint64_t t_b = leader_timer();
     bool first = true;
     while (true) {
@@ -2299,7 +2375,7 @@ __device__ void gcb_driver(Path& P, const rbf_gcb_args& a, const LoopScratch& s,
         save(RBF_EGROW, handover);
         return;
       }
-      const Best gb{__ldcg(&gbest[gk].err), __ldcg(&gbest[gk].pos)};
+      const Best gb = gk < ncache ? gcache[gk] : Best{__ldcg(&gbest[gk].err), __ldcg(&gbest[gk].pos)};
       if (gb.err > a.tol) {  // the run ends here: back to the one-cluster loop
         save(RBF_EGROW, handover);
         return;

@@ -425,7 +425,8 @@ class _LoopBuffers:
         L = t.empty(_tri(cap), dtype=t.float64, device=dev)
         Li = t.empty(_tri(cap), dtype=t.float64, device=dev)
         y = t.empty((cap, 3), dtype=t.float64, device=dev)
-        sup = t.empty((6, cap), dtype=t.float64, device=dev)  # SoA: x, y, z, wx, wy, wz
+        # SoA: x, y, z, wx, wy, wz, then the compensated weights' hi (3) and lo (3) rows
+        sup = t.empty((12, cap), dtype=t.float64, device=dev)
         sel = t.empty(cap, dtype=t.int32, device=dev)
         if n:
             L[: _tri(n)] = self.L[: _tri(n)]
