@@ -5,28 +5,30 @@ The reference's own unit tests (``/root/reference/pkg/tests``, §
 step 6) import ``rbfdeform`` and its submodules; this package answers every import
 on the hot path with this repository's modules:
 
-    rbfdeform, rbfdeform.core, .selection, .errors, .estimator, .metrics, .meshio
+    rbfdeform, rbfdeform.core, .selection, .errors, .estimator, .metrics, .meshio,
+    .cli, .deformers
         -> paper_2004_04817_b200 (and its submodules of the same names)
 
-Reference code outside the hot path is used only as test fixtures (the analytic
-bend-twist deformer and the desk-wing mesh generator the reference's conftest
-builds its cases with, and the surface-cell quality metrics test_metrics.py
-imports): ``rbfdeform.deformers`` and ``rbfdeform.synthetic`` are the reference's
-own files, and ``cell_quality`` / ``quality_report`` come from the reference's
-metrics.py, all copied next to this shim at staging time (not committed) and bound
-to this repository's ``errors`` / ``meshio`` / ``core``.
+Reference code outside the hot path is used only as test fixtures (the desk-wing
+mesh generator the reference's conftest builds its cases with, and the
+surface-cell quality metrics test_metrics.py imports): ``rbfdeform.synthetic`` is
+the reference's own file, and ``cell_quality`` / ``quality_report`` come from the
+reference's metrics.py, both copied next to this shim at staging time (not
+committed) and bound to this repository's ``errors`` / ``meshio`` / ``core``. The
+CLI's ``make-wing`` and quality sections are registered with them
+(``cli.MAKE_WING`` / ``cli.QUALITY_REPORT``).
 """
 
 import sys
 
 import paper_2004_04817_b200 as _P
 from paper_2004_04817_b200 import *  # noqa: F401,F403
-from paper_2004_04817_b200 import core, errors, estimator, meshio, metrics, selection  # noqa: F401
+from paper_2004_04817_b200 import cli, core, deformers, errors, estimator, meshio, metrics, selection  # noqa: F401
 
-for _name in ("core", "errors", "estimator", "meshio", "metrics", "selection"):
+for _name in ("cli", "core", "deformers", "errors", "estimator", "meshio", "metrics", "selection"):
     sys.modules[f"{__name__}.{_name}"] = getattr(_P, _name)
 
-from . import deformers, synthetic  # noqa: E402  (reference test fixtures)
+from . import synthetic  # noqa: E402  (reference test fixture)
 
 
 def _with_cell_quality(ours):
@@ -58,7 +60,11 @@ metrics = _with_cell_quality(_P.metrics)
 sys.modules[f"{__name__}.metrics"] = metrics
 cell_quality, quality_report = metrics.cell_quality, metrics.quality_report
 QualityReport = metrics.QualityReport
-from .deformers import BendTwistParams, SpanSineParams, bend_twist, prescribe, span_sine  # noqa: E402,F401
+from paper_2004_04817_b200.deformers import (  # noqa: E402,F401
+    BendTwistParams, SpanSineParams, bend_twist, prescribe, span_sine)
 from .synthetic import swept_wing_case, swept_wing_surface  # noqa: E402,F401
+
+cli.QUALITY_REPORT = quality_report
+cli.MAKE_WING = swept_wing_case
 
 BACKEND = "paper_2004_04817_b200 (sm_100a)"

@@ -5,13 +5,14 @@
 Copies (does not commit: ``build/`` is git-ignored but travels to the GPU box
 with the repo snapshot) the reference's test files for the hot-path modules --
 ``tests/test_core.py``, ``test_selection.py``, ``test_estimator.py``, plus
-``test_metrics.py`` and ``test_meshio.py`` for the §8(f) rows -- and its
-``conftest.py`` into ``build/conformance/``, with:
+``test_metrics.py``, ``test_meshio.py``, ``test_cli.py`` and ``test_deformers.py``
+for the §8(f) rows -- and its ``conftest.py`` into ``build/conformance/``, with:
 
 * ``build/conformance/rbfdeform/__init__.py`` = tools/conformance/rbfdeform_shim.py
   (the alias of ``rbfdeform`` to this package);
-* ``build/conformance/rbfdeform/{deformers,synthetic}.py`` = the reference's own
-  analytic-deformer and desk-wing generator (test fixtures outside the hot path);
+* ``build/conformance/rbfdeform/synthetic.py`` = the reference's own desk-wing
+  generator (a test fixture outside the hot path; also registered as the CLI's
+  ``make-wing``);
 * ``build/conformance/SOURCE`` recording where the files came from.
 
 tests/test_gpu_conformance.py runs the staged suite on the B200 (``-m gpu``) and
@@ -28,8 +29,8 @@ REPO = Path(__file__).resolve().parents[2]
 REF = Path("/root/reference/pkg")
 OUT = REPO / "build" / "conformance"
 TESTS = ["conftest.py", "test_core.py", "test_selection.py", "test_estimator.py", "test_metrics.py",
-         "test_meshio.py"]
-FIXTURES = ["deformers.py", "synthetic.py"]
+         "test_meshio.py", "test_cli.py", "test_deformers.py"]
+FIXTURES = ["synthetic.py"]
 
 
 def main():
