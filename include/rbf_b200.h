@@ -233,9 +233,12 @@ typedef struct rbf_gcb_state {
  *          distributed shared memory), the factor rows in L2 (n < 1024);
  *  CLUSTER one 16-CTA cluster, all state in global memory (L2);
  *  GRID    one CTA per SM (cooperative), all state in global memory.
- * AUTO picks MSG for group sizes up to 2048 (the kernel asks to resume in
- * SMEM once n reaches 448 and in CLUSTER once n reaches 1024) and GRID
- * above. */
+ * AUTO picks MSG for group sizes up to 2048 and GRID above. The kernel
+ * pauses (RBF_EGROW) and names the shape to resume in: MSG -> SMEM when n
+ * reaches 383 with group scans of at most 1.5e5 pairs (card * n), else ->
+ * GRID; SMEM -> GRID when n reaches 1023; any one-cluster shape -> GRID as
+ * soon as a group scan exceeds 4e5 pairs. CLUSTER runs only when forced
+ * (DESIGN.md §4.2). */
 enum { RBF_GCB_AUTO = 0, RBF_GCB_CLUSTER = 1, RBF_GCB_GRID = 2, RBF_GCB_SMEM = 3, RBF_GCB_MSG = 4 };
 
 typedef struct rbf_gcb_args {
