@@ -155,6 +155,21 @@ RBF_API int rbf_chol_append(double* L, double* Li, int64_t n, const double* row,
                     double* pivot2_host, void* scratch, size_t scratch_bytes,
                     void* stream);
 
+/* rbf_chol_append_points: rbf_chol_append for rows n0 .. n0+k-1 at once,
+ * the rows built on the device from the supports' coordinates (sup: device
+ * (n0+k, 3) AoS; row i = phi(|s_i - s_j| / radius), j <= i, the reference's
+ * kernel_matrix rounding, core.py:82-88) -- no host round trip between the
+ * rows (solve_support_weights core.py:268-281, metrics.error_history
+ * metrics.py:91-115). Stops at the first non-positive pivot: returns
+ * RBF_ENOTPD with *appended_host = rows appended before it (the state has
+ * order n0 + *appended_host) and *fail_pivot2_host its pivot^2. Synchronous
+ * (one host read at the end). L and Li must have room for order n0 + k.
+ * `scratch` holds rbf_chol_points_scratch_bytes(n0 + k + 1) bytes. */
+RBF_API size_t rbf_chol_points_scratch_bytes(int64_t n_total);
+RBF_API int rbf_chol_append_points(double* L, double* Li, int64_t n0, int64_t k, const double* sup,
+                                   double radius, int64_t* appended_host, double* fail_pivot2_host,
+                                   void* scratch, size_t scratch_bytes, void* stream);
+
 /* rbf_chol_solve (core.py:187-205): x = (L L^T)^-1 rhs for rhs (n, k)
  * row-major, k >= 1. out may alias rhs. */
 RBF_API int rbf_chol_solve(const double* L, const double* Li, int64_t n,

@@ -133,6 +133,11 @@ SIGNATURES = [
     ("rbf_best_fold", ctypes.c_int, [c_dp, ctypes.c_int64, c_dp, c_dp]),
     ("rbf_nearest", ctypes.c_int, [c_dp, ctypes.c_int64, c_dp, ctypes.c_int64, c_dp, c_dp]),
     ("rbf_chol_scratch_bytes", ctypes.c_size_t, [ctypes.c_int64]),
+    ("rbf_chol_points_scratch_bytes", ctypes.c_size_t, [ctypes.c_int64]),
+    ("rbf_chol_append_points", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                              ctypes.c_void_p, ctypes.c_double, ctypes.POINTER(ctypes.c_int64),
+                                              ctypes.POINTER(ctypes.c_double), ctypes.c_void_p, ctypes.c_size_t,
+                                              ctypes.c_void_p]),
     ("rbf_chol_append", ctypes.c_int,
      [c_dp, c_dp, ctypes.c_int64, c_dp, ctypes.POINTER(ctypes.c_double), c_dp, ctypes.c_size_t, c_dp]),
     ("rbf_chol_solve", ctypes.c_int,

@@ -184,6 +184,41 @@ class CholeskyState:
         self._n = n + 1
         return self
 
+    def _append_points(self, points, radius):
+        """Append the kernel rows of supports ``points[order:]`` against every
+        support before them (``points[:order]`` must be the supports already
+        factored), built on the device with the reference's kernel_matrix
+        rounding, in ONE device pass with no host round trip between rows
+        (rbf_chol_append_points). Raises NotPositiveDefiniteError at the first
+        non-positive pivot, with the rows before it kept."""
+        points = np.ascontiguousarray(points, dtype=float).reshape(-1, 3)
+        n0, total = self._n, len(points)
+        if total < n0:
+            raise DimensionMismatchError(f"{total} points for a factor of order {n0}")
+        if total == n0:
+            return self
+        lib = N.require_cuda()
+        t = N.torch()
+        self._reserve(total)
+        sup = _to_device(points)
+        nbytes = lib.rbf_chol_points_scratch_bytes(total + 1)
+        scratch = t.empty(nbytes, dtype=t.uint8, device=_device())
+        done = N.ctypes.c_int64(0)
+        piv = N.ctypes.c_double(0.0)
+        with N.launching("rbf_chol_append_points", kernels=7 * (total - n0)):
+            rc = lib.rbf_chol_append_points(N.dptr(self._L), N.dptr(self._Li), n0, total - n0, N.dptr(sup),
+                                            float(radius), N.ctypes.byref(done), N.ctypes.byref(piv),
+                                            N.dptr(scratch), nbytes, N.stream_ptr())
+        if rc == N.RBF_ENOTPD:
+            self._n = n0 + int(done.value)
+            raise NotPositiveDefiniteError(
+                f"pivot^2 = {piv.value:.3e} appending row {self._n}; "
+                "support nodes may coincide or be nearly coincident"
+            )
+        N.check(rc, "rbf_chol_append_points")
+        self._n = total
+        return self
+
     def solve(self, rhs):
         rhs = np.asarray(rhs, dtype=float)
         if rhs.shape[:1] != (self._n,):
@@ -269,8 +304,7 @@ def solve_support_weights(points, displacements, radius):
     points = np.asarray(points, dtype=float)
     displacements = np.asarray(displacements, dtype=float)
     state = CholeskyState()
-    for k in range(len(points)):
-        state.append(kernel_matrix(points[k : k + 1], points[: k + 1], radius)[0])
+    state._append_points(points, radius)  # the rows of the loop above, in one device pass
     return solve_weights(state, displacements)
 
 

@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdint>
 
+#include "rbf_common.cuh"
 #include "rbf_internal.h"
 #include "rbf_tri.cuh"
 
@@ -75,6 +76,56 @@ __global__ void k_pivot(const double* row, const double* c, int n, double* out) 
 // Write row n of L and Li once the pivot is accepted.
 __global__ void k_commit(double* L, double* Li, int n, const double* c, const double* u,
                          double l) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) {
+    L[tri_off(n) + j] = c[j];
+    Li[tri_off(n) + j] = -u[j] / l;
+  } else if (j == n) {
+    L[tri_off(n) + n] = l;
+    Li[tri_off(n) + n] = 1.0 / l;
+  }
+}
+
+// Batched appends (rbf_chol_append_points): the kernel row of support i
+// against supports 0..i with the reference's rounding (kernel_matrix,
+// core.py:82-88: phi(cdist / R), phi(0) = 1), skipped once an earlier row of
+// the batch failed.
+__global__ void k_exact_row(const double* sup, int i, double radius, const int* status, double* row) {
+  if (*status) return;
+  const double px = sup[3 * (int64_t)i], py = sup[3 * (int64_t)i + 1], pz = sup[3 * (int64_t)i + 2];
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= i; j += gridDim.x * blockDim.x)
+    row[j] = j == i ? 1.0 : phi_exact(cdist_exact(px, py, pz, sup[3 * (int64_t)j], sup[3 * (int64_t)j + 1],
+                                                  sup[3 * (int64_t)j + 2]), radius);
+}
+// pivot^2 as k_pivot; a non-positive one records (row, pivot^2) and stops the
+// rest of the batch (status = 1)
+__global__ void k_pivot_status(const double* row, const double* c, int n, double* piv, int* status,
+                               double* fail) {
+  if (*status) return;
+  double acc = 0.0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) acc = fma(c[j], c[j], acc);
+  acc = warp_sum(acc);
+  __shared__ double s[32];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    const double p2 = row[n] - t;
+    piv[0] = p2;
+    if (!(p2 > 0.0)) {
+      fail[0] = p2;
+      fail[1] = (double)n;
+      *status = 1;
+    }
+  }
+}
+// k_commit with l = sqrt(pivot^2) taken on the device (correctly rounded, as
+// the host's std::sqrt in rbf_chol_append)
+__global__ void k_commit_dev(double* L, double* Li, int n, const double* c, const double* u,
+                             const double* piv, const int* status) {
+  if (*status) return;
+  const double l = sqrt(piv[0]);
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < n) {
     L[tri_off(n) + j] = c[j];
@@ -186,5 +237,65 @@ extern "C" int rbf_chol_solve(const double* L, const double* Li, int64_t n64, co
     cols_fn(kc)(Li, n, t + c0, ld, y0 + c0, ld, 1.0, out + c0, ld, st);
   }
   RBF_LAUNCH_CHECK("chol solve");
+  return RBF_OK;
+}
+
+extern "C" size_t rbf_chol_points_scratch_bytes(int64_t n_total) {
+  const size_t v = ((size_t)(n_total < 1 ? 1 : n_total) * sizeof(double) + 255) & ~(size_t)255;
+  return 5 * v + 256;
+}
+
+// Append rows n0 .. n0+k-1 (supports sup[n0 .. n0+k) against every support
+// before them) with no host round trip between them: the same kernels as
+// rbf_chol_append per row, the pivot test on the device; a failing row stops
+// the batch (its kernels and every later row's return at once) and the host
+// reads (status, row, pivot^2) once at the end.
+extern "C" int rbf_chol_append_points(double* L, double* Li, int64_t n0, int64_t k, const double* sup,
+                                      double radius, int64_t* appended_host, double* fail_pivot2_host,
+                                      void* scratch, size_t scratch_bytes, void* stream) {
+  if (n0 < 0 || k < 0 || n0 + k >= INT32_MAX) return set_error(RBF_EARG, "bad order");
+  if (!(radius > 0.0)) return set_error(RBF_EARG, "radius must be positive");
+  if (appended_host) *appended_host = 0;
+  if (k == 0) return RBF_OK;
+  if (!L || !Li || !sup || !scratch) return set_error(RBF_EARG, "null pointer");
+  const int ntot = (int)(n0 + k);
+  if (scratch_bytes < rbf_chol_points_scratch_bytes(ntot + 1)) return set_error(RBF_EARG, "scratch too small");
+  cudaStream_t st = as_stream(stream);
+  const size_t v = ((size_t)(ntot + 1) * sizeof(double) + 255) & ~(size_t)255;
+  char* base = static_cast<char*>(scratch);
+  double* c0 = reinterpret_cast<double*>(base);
+  double* r = reinterpret_cast<double*>(base + v);
+  double* c = reinterpret_cast<double*>(base + 2 * v);
+  double* u = reinterpret_cast<double*>(base + 3 * v);
+  double* row = reinterpret_cast<double*>(base + 4 * v);
+  double* piv = reinterpret_cast<double*>(base + 5 * v);  // [0] pivot^2, [1..2] failing (pivot^2, row)
+  int* status = reinterpret_cast<int*>(base + 5 * v + 64);
+  RBF_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int), st));
+  for (int n = (int)n0; n < ntot; ++n) {
+    k_exact_row<<<(n + 256) / 256, 256, 0, st>>>(sup, n, radius, status, row);
+    if (n > 0) {
+      launch_rows<1>(Li, n, row, 1, nullptr, 0, 1.0, c0, 1, st);   // c0 = Li row
+      launch_rows<1>(L, n, c0, 1, row, 1, -1.0, r, 1, st);         // r = row - L c0
+      launch_rows<1>(Li, n, r, 1, c0, 1, 1.0, c, 1, st);           // c = c0 + Li r
+    }
+    k_pivot_status<<<1, 256, 0, st>>>(row, c, n, piv, status, piv + 1);
+    if (n > 0) launch_cols<1>(Li, n, c, 1, nullptr, 0, 1.0, u, 1, st);  // u = Li^T c
+    k_commit_dev<<<(n + 1 + 255) / 256, 256, 0, st>>>(L, Li, n, c, u, piv, status);
+  }
+  RBF_LAUNCH_CHECK("chol append points");
+  struct {
+    double fail[2];
+    int status;
+  } h{};
+  RBF_CUDA_TRY(cudaMemcpyAsync(&h.fail, piv + 1, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  RBF_CUDA_TRY(cudaMemcpyAsync(&h.status, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RBF_CUDA_TRY(cudaStreamSynchronize(st));
+  if (h.status) {
+    if (appended_host) *appended_host = (int64_t)h.fail[1] - n0;
+    if (fail_pivot2_host) *fail_pivot2_host = h.fail[0];
+    return set_error(RBF_ENOTPD, "pivot^2 = %.3e appending row %d; support nodes may coincide or be nearly coincident",
+                     h.fail[0], (int)h.fail[1]);
+  }
+  if (appended_host) *appended_host = k;
   return RBF_OK;
 }

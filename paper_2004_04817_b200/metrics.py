@@ -12,7 +12,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from .core import CholeskyState, SupportSet, _device, _to_device, _to_host, kernel_matrix
+from .core import CholeskyState, SupportSet, _device, _to_device, _to_host
 from .errors import EmptySupportSetError
 from .selection import _argmax_lowest_id, _errors_at
 
@@ -85,7 +85,8 @@ def error_history(boundary, support_nodes, radius, every=50):
     """Error summaries at prefixes of a support sequence (metrics.py:91-115).
 
     The reference re-factors every sampled prefix one-shot (``cho_factor``);
-    here the sequence is factored once by device appends and every prefix is
+    here the sequence is factored once by device appends (rows built on the
+    device, one host round trip for the whole sequence) and every prefix is
     solved with the leading block of that factor (a prefix of the packed
     triangles), then the boundary is scanned on the device. Same
     mathematics; agreement is at the factorisation's rounding level.
@@ -98,8 +99,7 @@ def error_history(boundary, support_nodes, radius, every=50):
     positions = np.searchsorted(boundary.indices, support_nodes)
     pts_all = boundary.points[positions]
     state = CholeskyState()
-    for k in range(total):
-        state.append(kernel_matrix(pts_all[k:k + 1], pts_all[:k + 1], radius)[0])
+    state._append_points(pts_all, radius)  # every row on the device, one host round trip
     out = []
     for n in counts:
         if n == 0:

@@ -342,11 +342,12 @@ def _argmax_lowest_id(errors, ids):
 
 # ------------------------------------------------------------ device scans
 def _errors_device(positions, boundary, support_points, weights, radius, want_errors=True):
-    """Fused device error scan + (err, lowest position) arg-max."""
+    """Fused device error scan + (err, lowest position) arg-max. The boundary
+    is uploaded per call unless it was staged (``stage_boundary``: then the
+    HBM copy is used and a per-group caller moves only the group's positions)."""
     lib = N.require_cuda()
     t = N.torch()
-    pts = _to_device(boundary.points)
-    disp = _to_device(boundary.disp)
+    pts, disp = _boundary_on_device(boundary)
     pos = _to_device(np.asarray(positions, dtype=np.int64), dtype=t.int64)
     sp = _to_device(support_points)
     w = _to_device(weights)

@@ -227,6 +227,31 @@ def test_cholesky_growth_and_random_spd(cuda, rng):
         assert np.abs(a @ st.solve(wide) - wide).max() <= 1e-9 * np.abs(wide).max()
 
 
+def test_cholesky_batched_device_rows_equal_row_appends(cuda, rng):
+    """rbf_chol_append_points (rows built on the device, one host round trip)
+    produces the factor of the per-row appends bit for bit, continues a
+    partly built factor, and stops at a coincident support with the rows
+    before it kept (reference core.py:153-185 semantics per row)."""
+    pts = rng.normal(size=(130, 3))
+    a = cuda.assemble_phi(pts, 2.5)
+    one = cuda.CholeskyState()
+    for k in range(130):
+        one.append(a[k, : k + 1])
+    batch = cuda.CholeskyState()._append_points(pts, 2.5)
+    assert batch.order == 130 and np.array_equal(batch.factor, one.factor)
+    part = cuda.CholeskyState()
+    for k in range(40):
+        part.append(a[k, : k + 1])
+    part._append_points(pts, 2.5)
+    assert np.array_equal(part.factor, one.factor)
+    bad = np.vstack([pts[:20], pts[7:8], pts[20:25]])
+    st = cuda.CholeskyState()
+    with pytest.raises(cuda.errors.NotPositiveDefiniteError, match="appending row 20"):
+        st._append_points(bad, 2.5)
+    assert st.order == 20 and np.array_equal(st.factor, one.factor[:20, :20])
+    assert st._append_points(bad[:20], 2.5).order == 20  # nothing to add
+
+
 def test_solve_support_weights_recovers(cuda, rng):
     pts = rng.normal(size=(20, 3)) * 2.0
     disp = rng.normal(size=(20, 3)) * 0.1
