@@ -34,3 +34,13 @@ if [ "${NCU:-1}" = 1 ]; then
   fi
   tail -n 1 gpurun_out/m_ncu_cfg1.log gpurun_out/m_ncu_cfg1_eval.log gpurun_out/m_ncu_cfg2.log
 fi
+# keep what comes back small (gpurun merges at most 64 MiB): per-report raw CSV
+# and the summary table on the box, then drop reports larger than 24 MiB
+for r in gpurun_out/m_prof_*.ncu-rep; do
+  [ -f "$r" ] || continue
+  ncu -i "$r" --page raw --csv > "${r%.ncu-rep}_raw.csv" 2>/dev/null
+  ncu -i "$r" --page details --csv > "${r%.ncu-rep}_details.csv" 2>/dev/null
+done
+python tools/ncu_summary.py gpurun_out/m_prof_*.ncu-rep > gpurun_out/m_ncu_summary.md 2>/dev/null
+find gpurun_out -name 'm_prof_*.ncu-rep' -size +24M -delete
+du -sh gpurun_out
