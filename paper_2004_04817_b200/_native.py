@@ -12,7 +12,9 @@ import numpy as np
 
 from .errors import NativeUnavailableError
 
-_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "librbf_b200.so"
+# RBF_LIB: an alternative build of the library (A/B experiments, tools/ab_build.sh)
+_LIB_PATH = (Path(os.environ["RBF_LIB"]) if os.environ.get("RBF_LIB")
+             else Path(__file__).resolve().parent / "_lib" / "librbf_b200.so")
 
 RBF_OK = 0
 RBF_EARG = 1
