@@ -236,6 +236,33 @@ __device__ __forceinline__ double row_dot(const double* arow, int len, XL xload,
   return warp_sum(acc);
 }
 
+// row_dot with x in shared memory: only the row is held in registers and x
+// is read from shared memory at the FMA (row_dot buffers both in registers).
+// configs[3] selection 326.7 -> 301.1 ms (the r / c / u products 10-20 %
+// faster; 16 and 32 row loads in flight per lane measure the same,
+// tools/sel_time.py). Same per-lane order as row_dot, so the same bits.
+#ifndef RBF_SX_BATCH
+#define RBF_SX_BATCH 16
+#endif
+template <int kB, typename XL>
+__device__ __forceinline__ double row_dot_sx(const double* arow, int len, XL xs, int lane) {
+  double acc = 0.0;
+  for (int j0 = 0; j0 < len; j0 += kB * kWarp) {
+    double av[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const int j = j0 + u * kWarp + lane;
+      av[u] = j < len ? __ldcg(arow + j) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const int j = j0 + u * kWarp + lane;
+      acc = fma(av[u], j < len ? xs(j) : 0.0, acc);
+    }
+  }
+  return warp_sum(acc);
+}
+
 enum AppendResult { kAccepted = 0, kRejectDup = 1, kRejectPivot = 2 };
 
 // Row phi(cdist(p, s_j) / R) of candidate p against the n supports with the
@@ -523,7 +550,8 @@ struct GlobalPath {
   // pre(v) -> POD: the finishing lane's operands of vector v, loaded
   // before the dot product so their L2 latency overlaps it
   template <bool kCols, class XL, class Pre, class Fin>
-  __device__ __forceinline__ void tri_gemv(const double* A, int n, XL xload, Pre pre, Fin finish) {
+  __device__ __forceinline__ void tri_gemv(const double* A, int n, XL xload, Pre pre, Fin finish,
+                                           bool x_smem = false) {
     const int lane = threadIdx.x & 31;
     const int G = gridDim.x;
     const int64_t cap = a.cap;
@@ -573,7 +601,8 @@ struct GlobalPath {
       auto xl = [&](int e) { return xload(v, e); };
       decltype(pre(0)) pf{};
       if (lane == 0) pf = pre(v);
-      const double acc = len > 1024 ? row_dot<16>(av, len, xl, lane) : row_dot<8>(av, len, xl, lane);
+      const double acc = x_smem ? row_dot_sx<RBF_SX_BATCH>(av, len, xl, lane)
+                                : len > 1024 ? row_dot<16>(av, len, xl, lane) : row_dot<8>(av, len, xl, lane);
       if (lane == 0) finish(v, acc, pf);
     }
   }
@@ -605,14 +634,14 @@ struct GlobalPath {
     // c0 = Li row
     auto no_pre = [](int) { return make_double4(0.0, 0.0, 0.0, 0.0); };
     tri_gemv<false>(a.Li, n, [&](int, int e) { return row[e]; }, no_pre,
-                    [&](int v, double acc, const double4&) { s.c0[v] = acc; });
+                    [&](int v, double acc, const double4&) { s.c0[v] = acc; }, n < kRowSmemMax);
     team.sync();
     pc.mark(2);
     // r = row - L c0
     const double* xs = stage_x(s.c0, n);
     tri_gemv<false>(a.L, n, [&](int, int e) { return xs ? xs[e] : __ldcg(s.c0 + e); },
                     no_pre,
-                    [&](int v, double acc, const double4&) { s.r[v] = row[v] - acc; });
+                    [&](int v, double acc, const double4&) { s.r[v] = row[v] - acc; }, xs != nullptr);
     team.sync();
     pc.mark(3);
     // c = c0 + Li r, with this CTA's partials of c.c and c.y
@@ -632,7 +661,8 @@ struct GlobalPath {
           pcy0 = fma(c, pf.y, pcy0);
           pcy1 = fma(c, pf.z, pcy1);
           pcy2 = fma(c, pf.w, pcy2);
-        });
+        },
+        xs != nullptr);
     Common& cm = sh.cm;
     if (lane == 0) {
       cm.wred[warp][0] = pcc;
@@ -708,7 +738,8 @@ struct GlobalPath {
             whi[k * (int64_t)cap + j] = h;
             wlo[k * (int64_t)cap + j] = lo;
           }
-        });
+        },
+        xs != nullptr);
     if (blockIdx.x == 0 && tid == 0) {
       Lirow[n] = inv_l;
       s.lic[col_off(n, cap)] = inv_l;
