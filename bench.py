@@ -359,10 +359,9 @@ def run_ours(args, rank, world, local):
 
     def device_step():
         """One step on device-resident inputs; returns (result or None, Nc)."""
-        if not shard:
-            res = P.gcb_select(boundary, cfg)
-            sp = torch.from_numpy(res.support.points).cuda()
-            sw = torch.from_numpy(res.support.weights).cuda()
+        if not shard:  # the volume kernel queued behind the loop (select_and_deform)
+            res, _ = P.select_and_deform(boundary, cfg, vol_d, out=out_d)
+            return res, len(res.support)
         else:
             res = _gcb_run(boundary, cfg, sweep=False) if rank == 0 else None
             sp, sw, _ = (multi.broadcast_support(res.support.points, res.support.weights) if rank == 0

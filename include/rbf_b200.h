@@ -303,6 +303,19 @@ RBF_API size_t rbf_gcb_scratch_bytes(int32_t nb, int32_t cap, int32_t ctas);
  * inel before the first call. */
 RBF_API int rbf_gcb_run(const rbf_gcb_args* args, void* stream);
 
+/* rbf_eval with the supports taken from a selection run's own buffers:
+ * `sup` = rbf_gcb_args.sup (SoA rows x, y, z, wx, wy, wz of capacity `cap`),
+ * the support count from state->n, read on the device. Meant to be queued
+ * on the selection's stream right behind rbf_gcb_run, before the host has
+ * read the result (the volume kernel then overlaps the host's unpacking of
+ * the selection: gcb_select + deform_points as one device sequence, the
+ * reference's cmd_deform, cli.py:158-182). Does nothing unless the loop
+ * finished (state->status == 1); the caller re-queues it otherwise. */
+RBF_API int rbf_eval_loop(const double* targets, int64_t n_targets, const double* sup, int64_t cap,
+                          const rbf_gcb_state* state, double radius, int deform, double* out,
+                          void* stream);
+
+
 /* ---------------------------------------------------------------------
  * Group partition on the host (replaces selection.py:177-185
  * `partition_boundary`'s arithmetic): numpy's PCG64 permutation of nb dealt

@@ -23,16 +23,31 @@ constexpr int kEvalTPT = 4;
 constexpr int kEvalTile = 128;
 enum EvalMode { kModeEval = 0, kModeDeform = 1, kModeError = 2 };
 
+// Where the supports are: element (support g, component c) of the points
+// and of the weights at ptr[g * row + c * comp] -- (n, 3) AoS arrays
+// (row 3, comp 1) or the selection loop's SoA buffer (row 1, comp cap);
+// with n_dev the support count is read on the device (a launch queued
+// behind the loop before the host knows it), and with status_dev the
+// launch does nothing unless the loop finished (status 1).
+struct SupLayout {
+  int64_t row = 3, comp = 1;
+  const int32_t* n_dev = nullptr;
+  const int32_t* status_dev = nullptr;
+};
+
 template <int MODE, int kEvalThreads = rbf::kEvalThreads, int kEvalTPT = rbf::kEvalTPT,
           int kEvalTile = rbf::kEvalTile, int kMinBlocks = 4>
 __global__ void __launch_bounds__(kEvalThreads, kMinBlocks)
 eval_kernel(const double* __restrict__ tpts, const double* __restrict__ tdisp,
             const int64_t* __restrict__ pos, int64_t nt,
             const double* __restrict__ spts, const double* __restrict__ sw, int nsup,
-            double inv_r, double* __restrict__ out, Best* __restrict__ partials) {
+            double inv_r, double* __restrict__ out, Best* __restrict__ partials, SupLayout lay = {}) {
   constexpr int kEvalTargetsPerBlock = kEvalThreads * kEvalTPT;
   __shared__ double4 s_a[kEvalTile];  // scaled x, y, z, wx
   __shared__ double2 s_b[kEvalTile];  // wy, wz
+  if (lay.status_dev && __ldcg(lay.status_dev) != 1) return;
+  if (lay.n_dev) nsup = __ldcg(lay.n_dev);
+  const int64_t srow = lay.row, scomp = lay.comp;
 
   const int64_t base = (int64_t)blockIdx.x * kEvalTargetsPerBlock + threadIdx.x;
   double px[kEvalTPT], py[kEvalTPT], pz[kEvalTPT];
@@ -58,10 +73,9 @@ eval_kernel(const double* __restrict__ tpts, const double* __restrict__ tdisp,
     const int cnt = min(kEvalTile, nsup - t0);
     __syncthreads();
     for (int j = threadIdx.x; j < cnt; j += kEvalThreads) {
-      const int g = t0 + j;
-      s_a[j] = make_double4(spts[3 * g] * inv_r, spts[3 * g + 1] * inv_r,
-                            spts[3 * g + 2] * inv_r, sw[3 * g]);
-      s_b[j] = make_double2(sw[3 * g + 1], sw[3 * g + 2]);
+      const int64_t g = (t0 + j) * srow;
+      s_a[j] = make_double4(spts[g] * inv_r, spts[g + scomp] * inv_r, spts[g + 2 * scomp] * inv_r, sw[g]);
+      s_b[j] = make_double2(sw[g + scomp], sw[g + 2 * scomp]);
     }
     __syncthreads();
 #pragma unroll 2
@@ -303,6 +317,36 @@ extern "C" int rbf_eval(const double* targets, int64_t n_targets, const double* 
   else
     launch_eval<kModeEval>(eval_variant(), targets, n_targets, sup_points, sup_weights, (int)n_sup, inv_r, out, s);
   RBF_LAUNCH_CHECK("eval_kernel");
+  return RBF_OK;
+}
+
+// The volume evaluation queued behind the selection loop on its stream, with
+// the supports and weights read from the loop's own buffers (SoA rows 0-5 of
+// rbf_gcb_args.sup, capacity `cap`) and their count from the loop state: the
+// host enqueues it before it has read the loop's result, so the volume
+// kernel runs while the host reads and unpacks the selection. A no-op (and
+// the caller re-runs it) unless the loop finished (state->status == 1).
+extern "C" int rbf_eval_loop(const double* targets, int64_t n_targets, const double* sup, int64_t cap,
+                             const rbf_gcb_state* state, double radius, int deform, double* out, void* stream) {
+  if (n_targets < 0 || cap < 1) return set_error(RBF_EARG, "bad size");
+  if (!(radius > 0.0)) return set_error(RBF_EARG, "radius must be positive, got %g", radius);
+  if (n_targets == 0) return RBF_OK;
+  if (!targets || !out || !sup || !state) return set_error(RBF_EARG, "null pointer");
+  SupLayout lay;
+  lay.row = 1;
+  lay.comp = cap;
+  lay.n_dev = &state->n;
+  lay.status_dev = &state->status;
+  constexpr int NT = 128, TPT = 6;
+  const int64_t nblk = (n_targets + NT * TPT - 1) / (NT * TPT);
+  cudaStream_t s = as_stream(stream);
+  if (deform)
+    eval_kernel<kModeDeform, NT, TPT, 128, 3><<<(unsigned)nblk, NT, 0, s>>>(
+        targets, nullptr, nullptr, n_targets, sup, sup + 3 * cap, 0, 1.0 / radius, out, nullptr, lay);
+  else
+    eval_kernel<kModeEval, NT, TPT, 128, 3><<<(unsigned)nblk, NT, 0, s>>>(
+        targets, nullptr, nullptr, n_targets, sup, sup + 3 * cap, 0, 1.0 / radius, out, nullptr, lay);
+  RBF_LAUNCH_CHECK("eval_kernel (loop supports)");
   return RBF_OK;
 }
 

@@ -286,6 +286,10 @@ def _take_buffers(nb, cap, rec_cap, ctas):
         buf = free.pop() if free else None
     if buf is None:
         return key, _LoopBuffers(nb, cap, rec_cap, ctas)
+    busy = getattr(buf, "busy", None)
+    if busy is not None:  # a kernel queued by read_all(then) may still read the buffers
+        N.torch().cuda.current_stream().wait_event(busy)
+        buf.busy = None
     buf.reset()
     return key, buf
 
@@ -446,9 +450,11 @@ class _LoopBuffers:
             self._host = self.t.empty(sz, dtype=self.t.uint8, pin_memory=True)
         return self._host
 
-    def read_all(self):
+    def read_all(self, then=None):
         """Async copies of state, sel, weight rows and records into one
-        pinned buffer, one synchronisation; returns (state, host bytes)."""
+        pinned buffer, one synchronisation; returns (state, host bytes).
+        ``then(self)`` is queued on the stream behind the copies (the host
+        waits for the copies only, not for it)."""
         t = self.t
         host = self._staging()
         ss = N.ctypes.sizeof(N.GcbState)
@@ -460,7 +466,13 @@ class _LoopBuffers:
         host[o1:o2].copy_(self.sel.view(t.uint8), non_blocking=True)
         host[o2:o3].copy_(self.sup[3:6].reshape(-1).view(t.uint8), non_blocking=True)
         host[o3:o4].copy_(self.records.reshape(-1), non_blocking=True)
-        t.cuda.current_stream().synchronize()
+        copied = t.cuda.Event()
+        copied.record()
+        if then is not None:  # queued behind the copies: runs while the host unpacks
+            then(self)
+            self.busy = t.cuda.Event()
+            self.busy.record()
+        copied.synchronize()
         hb = host.numpy()
         self._offsets = (o1, o2, o3)
         return N.GcbState.from_buffer_copy(hb[:ss].tobytes()), hb
@@ -505,7 +517,7 @@ def gcb_select(boundary, config):
     return _gcb_run(boundary, config)
 
 
-def _gcb_run(boundary, config, mode=None, phases=None, sweep=True):
+def _gcb_run(boundary, config, mode=None, phases=None, sweep=True, then=None):
     """The device loop. ``sweep=False`` stops before the final sweep
     (RBF_GCB_NO_SWEEP; multi.gcb_select shards it over ranks): the returned
     history's ``final_sweep`` then carries the iteration number, counters and
@@ -576,7 +588,7 @@ def _gcb_run(boundary, config, mode=None, phases=None, sweep=True):
         N.check(rc, "rbf_gcb_run")
         # state, selection, weights and records in one staged read (the kernel
         # is stream-ordered before the copies): one synchronisation per launch
-        st, host = buf.read_all()
+        st, host = buf.read_all(then)
         if st.status == N.STATUS_DONE:
             break
         if st.status == N.RBF_ENOTPD:
@@ -647,6 +659,42 @@ def _gcb_run(boundary, config, mode=None, phases=None, sweep=True):
         support=support, history=history,
         converged=(float(fin["local_max"]) <= config.tol) if sweep else None,
     )
+
+
+def select_and_deform(boundary, config, points, out=None):
+    """gcb_select followed by deform_points of ``points`` over the selected
+    support set, as one device sequence (the reference's cmd_deform,
+    cli.py:158-182, and RBFMeshDeformer's fit + transform). With ``points`` a
+    CUDA tensor (n, 3) float64 the volume kernel is queued on the selection's
+    stream right behind the loop, reading the supports, weights and their
+    count from the loop's own buffers (rbf_eval_loop), so it runs while the
+    host reads back and unpacks the selection; ``out`` (or a new tensor)
+    receives the moved points when the stream reaches it. Returns
+    (SelectionResult, moved). Host (numpy) points: gcb_select then
+    deform_points. Same values as the two calls."""
+    from .core import deform_points
+
+    t = N.torch()
+    if not (isinstance(points, t.Tensor) and points.is_cuda):
+        res = gcb_select(boundary, config)
+        return res, deform_points(points, res.support, config.radius)
+    if config.radius <= 0:
+        raise ValueError(f"radius must be positive, got {config.radius}")
+    pts = points.reshape(-1, 3)
+    if pts.dtype != t.float64 or not pts.is_contiguous():
+        pts = pts.to(t.float64).contiguous()
+    if out is None:
+        out = t.empty_like(pts)
+    n = pts.shape[0]
+    lib = N.require_cuda()
+
+    def then(buf):
+        with N.launching("rbf_eval", kernels=1 if n else 0):
+            rc = lib.rbf_eval_loop(N.dptr(pts), n, buf.sup.data_ptr(), buf.cap, buf.state.data_ptr(),
+                                   float(config.radius), 1, N.dptr(out), N.stream_ptr())
+        N.check(rc, "rbf_eval_loop")
+
+    return _gcb_run(boundary, config, then=then), out
 
 
 def greedy_select(boundary, config):

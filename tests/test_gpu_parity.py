@@ -411,6 +411,40 @@ def test_selection_growth_path(cuda, monkeypatch):
     assert rel(res.support.weights, g["weights"]) <= 1e-9
 
 
+def test_select_and_deform_equals_the_two_calls(cuda, monkeypatch):
+    """The fused device sequence (volume kernel queued behind the loop, supports
+    read from the loop's buffers) gives bitwise the result of gcb_select followed
+    by deform_points -- also when the loop pauses and resumes (tiny capacity:
+    the early-queued volume launches are no-ops and the last one does the work)
+    and across a MSG -> GRID hand-over (configs[2]-sized groups)."""
+    import torch
+    from paper_2004_04817_b200 import selection as S
+
+    wl = W.config(0, nv=30_000)
+    b = cuda.BoundarySet(np.arange(wl.nb), wl.points, wl.disp)
+    cfg = cuda.SelectionConfig(radius=wl.radius, tol=wl.tol, max_supports=wl.nb, m=8)
+    vol = torch.from_numpy(wl.volume).cuda()
+    ref = cuda.gcb_select(b, cfg)
+    moved_ref = cuda.deform_points(wl.volume, ref.support, wl.radius)
+    res, moved = cuda.select_and_deform(b, cfg, vol)
+    assert np.array_equal(res.support.nodes, ref.support.nodes)
+    assert np.array_equal(moved.cpu().numpy(), moved_ref)
+    monkeypatch.setattr(S, "_initial_capacity", lambda config, nb: 8)
+    res2, moved2 = cuda.select_and_deform(b, cfg, vol)
+    assert np.array_equal(res2.support.nodes, ref.support.nodes)
+    assert np.array_equal(moved2.cpu().numpy(), moved_ref)
+    monkeypatch.undo()
+    wl2 = W.structured_wing(n_span=60, n_section=200, nv=20_000, m=48, name="cfg2s")
+    b2 = cuda.BoundarySet(np.arange(wl2.nb), wl2.points, wl2.disp)
+    cfg2 = cuda.SelectionConfig(radius=wl2.radius, tol=wl2.tol, max_supports=wl2.nb, m=48)
+    r2 = cuda.gcb_select(b2, cfg2)
+    f2, m2 = cuda.select_and_deform(b2, cfg2, torch.from_numpy(wl2.volume).cuda())
+    assert np.array_equal(f2.support.nodes, r2.support.nodes)
+    assert np.array_equal(m2.cpu().numpy(), cuda.deform_points(wl2.volume, r2.support, wl2.radius))
+    h, hm = cuda.select_and_deform(b, cfg, wl.volume)  # host points: the two calls
+    assert np.array_equal(hm, moved_ref)
+
+
 def test_selection_edge_cases(cuda, rng):
     E = cuda.errors
     # huge tolerance: the seeds only, converged
