@@ -408,8 +408,11 @@ def run_ours(args, rank, world, local):
         with S._cache_lock:
             S._part_cache.clear()
         b_host = P.BoundarySet(np.arange(wl.nb), wl.points, wl.disp)
-        sup = (multi.gcb_select(b_host, cfg) if shard else P.gcb_select(b_host, cfg)).support
-        return sup, P.deform_points(vol, sup, wl.radius)
+        if shard:
+            sup = multi.gcb_select(b_host, cfg).support
+            return sup, P.deform_points(vol, sup, wl.radius)
+        res, moved = P.select_and_deform(b_host, cfg, vol)  # volume pipeline queued behind the loop
+        return res.support, moved
 
     e2e_times = []
     for i in range(args.warmup + args.steps):

@@ -125,6 +125,9 @@ SIGNATURES = [
     ("rbf_eval_loop", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
                                      ctypes.c_void_p, ctypes.c_double, ctypes.c_int, ctypes.c_void_p,
                                      ctypes.c_void_p]),
+    ("rbf_eval_host_loop", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
+                                          ctypes.c_void_p, ctypes.c_double, ctypes.c_int, ctypes.c_void_p,
+                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
     ("rbf_eval_host", ctypes.c_int,
      [c_dp, ctypes.c_int64, c_dp, c_dp, ctypes.c_int64, ctypes.c_double, ctypes.c_int, c_dp, c_dp, c_dp,
       ctypes.c_int, c_dp]),

@@ -372,14 +372,9 @@ struct PipeStreams {
 };
 }  // namespace
 
-extern "C" int rbf_eval_host(const double* host_targets, int64_t n_targets, const double* sup_points,
-                             const double* sup_weights, int64_t n_sup, double radius, int deform,
-                             double* dev_in, double* dev_out, double* host_out, int chunks, void* stream) {
-  if (n_targets < 0 || n_sup < 0) return set_error(RBF_EARG, "negative size");
-  if (!(radius > 0.0)) return set_error(RBF_EARG, "radius must be positive, got %g", radius);
-  if (n_targets == 0) return RBF_OK;
-  if (!host_targets || !host_out || !dev_in || !dev_out || (n_sup > 0 && (!sup_points || !sup_weights)))
-    return set_error(RBF_EARG, "null pointer");
+template <class Launch>
+static int eval_pipeline(const double* host_targets, int64_t n_targets, double* dev_in, double* dev_out,
+                         double* host_out, int chunks, void* stream, Launch launch_chunk) {
   if (chunks < 1) chunks = 1;
   if (chunks > 63) chunks = 63;  // events 3c+1, 3c+2 per chunk; 191 marks the end
   static thread_local PipeStreams ps;
@@ -443,8 +438,7 @@ extern "C" int rbf_eval_host(const double* host_targets, int64_t n_targets, cons
     RBF_CUDA_TRY(cudaMemcpyAsync(dev_in + 3 * lo, host_targets + 3 * lo, 24 * cnt, cudaMemcpyHostToDevice, ps.in));
     RBF_CUDA_TRY(cudaEventRecord(in_done, ps.in));
     RBF_CUDA_TRY(cudaStreamWaitEvent(cs, in_done, 0));
-    const int rc = rbf_eval(dev_in + 3 * lo, cnt, sup_points, sup_weights, n_sup, radius, deform,
-                            dev_out + 3 * lo, cs);
+    const int rc = launch_chunk(dev_in + 3 * lo, cnt, dev_out + 3 * lo, cs);
     if (rc != RBF_OK) return rc;
     RBF_CUDA_TRY(cudaEventRecord(k_done, cs));
     RBF_CUDA_TRY(cudaStreamWaitEvent(ps.out, k_done, 0));
@@ -470,6 +464,38 @@ extern "C" int rbf_eval_host(const double* host_targets, int64_t n_targets, cons
   RBF_CUDA_TRY(cudaEventRecord(ps.ev[3 * 63 + 2], ps.out));
   RBF_CUDA_TRY(cudaStreamWaitEvent(compute, ps.ev[3 * 63 + 2], 0));
   return RBF_OK;
+}
+
+extern "C" int rbf_eval_host(const double* host_targets, int64_t n_targets, const double* sup_points,
+                             const double* sup_weights, int64_t n_sup, double radius, int deform,
+                             double* dev_in, double* dev_out, double* host_out, int chunks, void* stream) {
+  if (n_targets < 0 || n_sup < 0) return set_error(RBF_EARG, "negative size");
+  if (!(radius > 0.0)) return set_error(RBF_EARG, "radius must be positive, got %g", radius);
+  if (n_targets == 0) return RBF_OK;
+  if (!host_targets || !host_out || !dev_in || !dev_out || (n_sup > 0 && (!sup_points || !sup_weights)))
+    return set_error(RBF_EARG, "null pointer");
+  return eval_pipeline(host_targets, n_targets, dev_in, dev_out, host_out, chunks, stream,
+                       [&](const double* in, int64_t cnt, double* out, cudaStream_t cs) {
+                         return rbf_eval(in, cnt, sup_points, sup_weights, n_sup, radius, deform, out, cs);
+                       });
+}
+
+// rbf_eval_host with the supports read from a selection run's buffers on
+// the device (rbf_eval_loop): the whole chunked copy / kernel / copy
+// pipeline is queued behind the selection loop before the host has read
+// its result. The kernels do nothing unless the loop finished; the copies
+// always run.
+extern "C" int rbf_eval_host_loop(const double* host_targets, int64_t n_targets, const double* sup, int64_t cap,
+                                  const rbf_gcb_state* state, double radius, int deform, double* dev_in,
+                                  double* dev_out, double* host_out, int chunks, void* stream) {
+  if (n_targets < 0 || cap < 1) return set_error(RBF_EARG, "bad size");
+  if (!(radius > 0.0)) return set_error(RBF_EARG, "radius must be positive, got %g", radius);
+  if (n_targets == 0) return RBF_OK;
+  if (!host_targets || !host_out || !dev_in || !dev_out || !sup || !state) return set_error(RBF_EARG, "null pointer");
+  return eval_pipeline(host_targets, n_targets, dev_in, dev_out, host_out, chunks, stream,
+                       [&](const double* in, int64_t cnt, double* out, cudaStream_t cs) {
+                         return rbf_eval_loop(in, cnt, sup, cap, state, radius, deform, out, cs);
+                       });
 }
 
 // Error scans use the volume kernel's launch shape (128 threads x 6 rows, 3

@@ -468,8 +468,9 @@ class _LoopBuffers:
         host[o3:o4].copy_(self.records.reshape(-1), non_blocking=True)
         copied = t.cuda.Event()
         copied.record()
+        self.then_queued = False
         if then is not None:  # queued behind the copies: runs while the host unpacks
-            then(self)
+            self.then_queued = bool(then(self))
             self.busy = t.cuda.Event()
             self.busy.record()
         copied.synchronize()
@@ -588,7 +589,8 @@ def _gcb_run(boundary, config, mode=None, phases=None, sweep=True, then=None):
         N.check(rc, "rbf_gcb_run")
         # state, selection, weights and records in one staged read (the kernel
         # is stream-ordered before the copies): one synchronisation per launch
-        st, host = buf.read_all(then)
+        st, host = buf.read_all(None if then is None else (lambda b, mode=args.mode: then(b, mode)))
+        then_done = buf.then_queued and st.status == N.STATUS_DONE
         if st.status == N.STATUS_DONE:
             break
         if st.status == N.RBF_ENOTPD:
@@ -655,46 +657,85 @@ def _gcb_run(boundary, config, mode=None, phases=None, sweep=True, then=None):
     history.device_mode = {N.GCB_CLUSTER: "cluster", N.GCB_GRID: "grid", N.GCB_SMEM: "smem",
                            N.GCB_MSG: "msg"}[args.mode]
     support = SupportSet(nodes=idx[sel], points=boundary.points[sel], weights=weights)
-    return SelectionResult(
+    result = SelectionResult(
         support=support, history=history,
         converged=(float(fin["local_max"]) <= config.tol) if sweep else None,
     )
+    if then is not None:
+        result._then_done = then_done  # the queued follow-up ran on the final state
+    return result
 
 
 def select_and_deform(boundary, config, points, out=None):
     """gcb_select followed by deform_points of ``points`` over the selected
     support set, as one device sequence (the reference's cmd_deform,
-    cli.py:158-182, and RBFMeshDeformer's fit + transform). With ``points`` a
-    CUDA tensor (n, 3) float64 the volume kernel is queued on the selection's
-    stream right behind the loop, reading the supports, weights and their
-    count from the loop's own buffers (rbf_eval_loop), so it runs while the
-    host reads back and unpacks the selection; ``out`` (or a new tensor)
-    receives the moved points when the stream reaches it. Returns
-    (SelectionResult, moved). Host (numpy) points: gcb_select then
-    deform_points. Same values as the two calls."""
-    from .core import deform_points
+    cli.py:158-182, and RBFMeshDeformer's fit + transform): the volume work is
+    queued on the selection's stream right behind the loop, reading the
+    supports, weights and their count from the loop's own buffers on the
+    device, so it runs while the host reads back and unpacks the selection.
+
+    * ``points`` a CUDA tensor (n, 3): one volume kernel (rbf_eval_loop);
+      ``out`` (or a new tensor) receives the moved points in stream order.
+    * ``points`` host (n, 3) array: the chunked copy / kernel / copy pipeline
+      (rbf_eval_host_loop) into a pinned host result, queued when the loop
+      runs in a one-cluster shape (it then finishes in the same call);
+      otherwise the two calls one after the other.
+
+    Returns (SelectionResult, moved). Bitwise the values of the two calls."""
+    from .core import _PIPELINE_CHUNKS, _device, deform_points
 
     t = N.torch()
-    if not (isinstance(points, t.Tensor) and points.is_cuda):
-        res = gcb_select(boundary, config)
-        return res, deform_points(points, res.support, config.radius)
     if config.radius <= 0:
         raise ValueError(f"radius must be positive, got {config.radius}")
-    pts = points.reshape(-1, 3)
-    if pts.dtype != t.float64 or not pts.is_contiguous():
-        pts = pts.to(t.float64).contiguous()
-    if out is None:
-        out = t.empty_like(pts)
-    n = pts.shape[0]
     lib = N.require_cuda()
+    on_device = isinstance(points, t.Tensor) and points.is_cuda
+    if on_device:
+        pts = points.reshape(-1, 3)
+        if pts.dtype != t.float64 or not pts.is_contiguous():
+            pts = pts.to(t.float64).contiguous()
+        if out is None:
+            out = t.empty_like(pts)
+    else:
+        host = np.ascontiguousarray(np.asarray(points, dtype=np.float64).reshape(-1, 3))
+        pts = t.from_numpy(host)
+        dev_in = t.empty(pts.shape, dtype=t.float64, device=_device())
+        dev_out = t.empty_like(dev_in)
+        out = t.empty(pts.shape, dtype=t.float64, pin_memory=True)
+    n = pts.shape[0]
+    if n == 0:
+        res = gcb_select(boundary, config)
+        return res, (out if on_device else out.numpy())
 
-    def then(buf):
-        with N.launching("rbf_eval", kernels=1 if n else 0):
-            rc = lib.rbf_eval_loop(N.dptr(pts), n, buf.sup.data_ptr(), buf.cap, buf.state.data_ptr(),
-                                   float(config.radius), 1, N.dptr(out), N.stream_ptr())
-        N.check(rc, "rbf_eval_loop")
+    def then(buf, mode):
+        if on_device:
+            with N.launching("rbf_eval", kernels=1):
+                rc = lib.rbf_eval_loop(N.dptr(pts), n, buf.sup.data_ptr(), buf.cap, buf.state.data_ptr(),
+                                       float(config.radius), 1, N.dptr(out), N.stream_ptr())
+            N.check(rc, "rbf_eval_loop")
+            return True
+        if mode not in (N.GCB_MSG, N.GCB_SMEM):
+            return False  # a GRID run pauses for capacity: the copies would be wasted
+        with N.launching("rbf_eval", kernels=_PIPELINE_CHUNKS):
+            rc = lib.rbf_eval_host_loop(pts.data_ptr(), n, buf.sup.data_ptr(), buf.cap, buf.state.data_ptr(),
+                                        float(config.radius), 1, N.dptr(dev_in), N.dptr(dev_out),
+                                        out.data_ptr(), _PIPELINE_CHUNKS, N.stream_ptr())
+        N.check(rc, "rbf_eval_host_loop")
+        return True
 
-    return _gcb_run(boundary, config, then=then), out
+    res = _gcb_run(boundary, config, then=then)
+    if not getattr(res, "_then_done", False):  # the loop finished in a round without it
+        if on_device:
+            from .core import eval_device
+
+            sp = t.from_numpy(np.ascontiguousarray(res.support.points)).to(pts.device)
+            sw = t.from_numpy(np.ascontiguousarray(res.support.weights)).to(pts.device)
+            eval_device(pts, sp, sw, config.radius, deform=True, out=out)
+            return res, out
+        return res, deform_points(host, res.support, config.radius)
+    if on_device:
+        return res, out
+    t.cuda.current_stream().synchronize()
+    return res, out.numpy()
 
 
 def greedy_select(boundary, config):

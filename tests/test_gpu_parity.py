@@ -441,8 +441,13 @@ def test_select_and_deform_equals_the_two_calls(cuda, monkeypatch):
     f2, m2 = cuda.select_and_deform(b2, cfg2, torch.from_numpy(wl2.volume).cuda())
     assert np.array_equal(f2.support.nodes, r2.support.nodes)
     assert np.array_equal(m2.cpu().numpy(), cuda.deform_points(wl2.volume, r2.support, wl2.radius))
-    h, hm = cuda.select_and_deform(b, cfg, wl.volume)  # host points: the two calls
-    assert np.array_equal(hm, moved_ref)
+    h, hm = cuda.select_and_deform(b, cfg, wl.volume)  # host points: pipeline behind the loop
+    assert getattr(h, "_then_done", False) and np.array_equal(hm, moved_ref)
+    pinned = torch.from_numpy(wl.volume.copy()).pin_memory().numpy()
+    h, hm = cuda.select_and_deform(b, cfg, pinned)
+    assert np.array_equal(hm, moved_ref) and np.array_equal(h.support.nodes, ref.support.nodes)
+    h3, hm3 = cuda.select_and_deform(b2, cfg2, wl2.volume)  # MSG -> GRID: the two calls
+    assert np.array_equal(hm3, cuda.deform_points(wl2.volume, r2.support, wl2.radius))
 
 
 def test_selection_edge_cases(cuda, rng):
