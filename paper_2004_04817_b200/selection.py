@@ -706,6 +706,8 @@ def select_and_deform(boundary, config, points, out=None):
         res = gcb_select(boundary, config)
         return res, (out if on_device else out.numpy())
 
+    staged = [None]
+
     def then(buf, mode):
         if on_device:
             with N.launching("rbf_eval", kernels=1):
@@ -715,8 +717,17 @@ def select_and_deform(boundary, config, points, out=None):
             return True
         if mode not in (N.GCB_MSG, N.GCB_SMEM):
             return False  # a GRID run pauses for capacity: the copies would be wasted
+        src = pts
+        if not src.is_pinned():
+            # pageable input: staged into pinned memory by the host while the
+            # loop runs on the device (torch's multi-threaded copy), so the
+            # pipeline's copies are asynchronous DMA
+            if staged[0] is None:
+                staged[0] = t.empty(pts.shape, dtype=t.float64, pin_memory=True)
+                staged[0].copy_(pts)
+            src = staged[0]
         with N.launching("rbf_eval", kernels=_PIPELINE_CHUNKS):
-            rc = lib.rbf_eval_host_loop(pts.data_ptr(), n, buf.sup.data_ptr(), buf.cap, buf.state.data_ptr(),
+            rc = lib.rbf_eval_host_loop(src.data_ptr(), n, buf.sup.data_ptr(), buf.cap, buf.state.data_ptr(),
                                         float(config.radius), 1, N.dptr(dev_in), N.dptr(dev_out),
                                         out.data_ptr(), _PIPELINE_CHUNKS, N.stream_ptr())
         N.check(rc, "rbf_eval_host_loop")
