@@ -58,6 +58,10 @@ constexpr int64_t kClusterScanPairs = 400000;  // per group scan, see gcb_driver
 constexpr int64_t kSmemScanPairs = 150000;
 constexpr int kMsgDefaultClusters = 1;         // MSG path: clusters sharing the scans
 constexpr int kNone = 0x7fffffff;
+#ifndef RBF_PAIR_ROWS
+#define RBF_PAIR_ROWS 1
+#endif
+constexpr bool kPairRows = RBF_PAIR_ROWS != 0;  // GlobalPath::tri_gemv: complementary vectors per warp
 // internal rbf_gcb_args.flags bits (set by rbf_gcb_run on its own copy)
 constexpr int kFlagTailSweep = 1 << 16;  // one-cluster launch: stop before the final sweep,
                                          // which a whole-GPU tail launch runs
@@ -595,7 +599,7 @@ struct GlobalPath {
       return;
     }
     const int gw = blockIdx.x * kLoopWarps + (threadIdx.x >> 5), nw = G * kLoopWarps;
-    for (int v = gw; v < n; v += nw) {
+    auto one = [&](int v) {
       const double* av = A + (kCols ? col_off(v, cap) : tri_off(v));
       const int len = kCols ? n - v : v + 1;
       auto xl = [&](int e) { return xload(v, e); };
@@ -604,6 +608,23 @@ struct GlobalPath {
       const double acc = x_smem ? row_dot_sx<RBF_SX_BATCH>(av, len, xl, lane)
                                 : len > 1024 ? row_dot<16>(av, len, xl, lane) : row_dot<8>(av, len, xl, lane);
       if (lane == 0) finish(v, acc, pf);
+    };
+    // More vectors than warps: a warp takes vectors p and n-1-p (n+1 entries
+    // together), so every warp streams the same amount -- with v, v + nw
+    // (the lengths of a triangle's vectors grow with v) the heaviest warps
+    // read ~1.5x the mean and every product waits for them. One call site of
+    // the dot product (a second one spills the loop kernel's registers).
+    const bool pair = kPairRows && n > nw;
+    const int lim = pair ? (n + 1) >> 1 : n;
+    for (int p = gw, k = 0; p < lim;) {
+      const int v = k ? n - 1 - p : p;
+      if (!k || v != p) one(v);
+      if (pair && !k) {
+        k = 1;
+      } else {
+        k = 0;
+        p += nw;
+      }
     }
   }
 
