@@ -317,7 +317,9 @@ RBF_API int rbf_eval_loop(const double* targets, int64_t n_targets, const double
 /* rbf_eval_host (host targets, chunked copy / kernel / copy pipeline) with
  * the supports of rbf_eval_loop: the selection's result goes straight into
  * the volume pipeline queued behind the loop. The copies always run; the
- * kernels only if the loop finished. */
+ * kernels only if the loop finished. host_targets == NULL: the targets are
+ * already in dev_in (the caller copied them ahead, in stream order, e.g.
+ * while the loop ran), and only the kernels and the result copies run. */
 RBF_API int rbf_eval_host_loop(const double* host_targets, int64_t n_targets, const double* sup,
                                int64_t cap, const rbf_gcb_state* state, double radius, int deform,
                                double* dev_in, double* dev_out, double* host_out, int chunks,

@@ -372,6 +372,8 @@ struct PipeStreams {
 };
 }  // namespace
 
+// host_targets == nullptr: the targets are already in dev_in (copied there
+// ahead of time by the caller, in stream order): only kernel + D2H per chunk
 template <class Launch>
 static int eval_pipeline(const double* host_targets, int64_t n_targets, double* dev_in, double* dev_out,
                          double* host_out, int chunks, void* stream, Launch launch_chunk) {
@@ -435,9 +437,11 @@ static int eval_pipeline(const double* host_targets, int64_t n_targets, double* 
     const int64_t cnt = sizes[c];
     cudaEvent_t in_done = ps.ev[3 * c + 1], k_done = ps.ev[3 * c + 2];
     cudaStream_t cs = ps.comp[c % kPipeCompute];
-    RBF_CUDA_TRY(cudaMemcpyAsync(dev_in + 3 * lo, host_targets + 3 * lo, 24 * cnt, cudaMemcpyHostToDevice, ps.in));
-    RBF_CUDA_TRY(cudaEventRecord(in_done, ps.in));
-    RBF_CUDA_TRY(cudaStreamWaitEvent(cs, in_done, 0));
+    if (host_targets) {
+      RBF_CUDA_TRY(cudaMemcpyAsync(dev_in + 3 * lo, host_targets + 3 * lo, 24 * cnt, cudaMemcpyHostToDevice, ps.in));
+      RBF_CUDA_TRY(cudaEventRecord(in_done, ps.in));
+      RBF_CUDA_TRY(cudaStreamWaitEvent(cs, in_done, 0));
+    }
     const int rc = launch_chunk(dev_in + 3 * lo, cnt, dev_out + 3 * lo, cs);
     if (rc != RBF_OK) return rc;
     RBF_CUDA_TRY(cudaEventRecord(k_done, cs));
@@ -491,7 +495,7 @@ extern "C" int rbf_eval_host_loop(const double* host_targets, int64_t n_targets,
   if (n_targets < 0 || cap < 1) return set_error(RBF_EARG, "bad size");
   if (!(radius > 0.0)) return set_error(RBF_EARG, "radius must be positive, got %g", radius);
   if (n_targets == 0) return RBF_OK;
-  if (!host_targets || !host_out || !dev_in || !dev_out || !sup || !state) return set_error(RBF_EARG, "null pointer");
+  if (!host_out || !dev_in || !dev_out || !sup || !state) return set_error(RBF_EARG, "null pointer");
   return eval_pipeline(host_targets, n_targets, dev_in, dev_out, host_out, chunks, stream,
                        [&](const double* in, int64_t cnt, double* out, cudaStream_t cs) {
                          return rbf_eval_loop(in, cnt, sup, cap, state, radius, deform, out, cs);

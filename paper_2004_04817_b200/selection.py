@@ -676,10 +676,12 @@ def select_and_deform(boundary, config, points, out=None):
 
     * ``points`` a CUDA tensor (n, 3): one volume kernel (rbf_eval_loop);
       ``out`` (or a new tensor) receives the moved points in stream order.
-    * ``points`` host (n, 3) array: the chunked copy / kernel / copy pipeline
-      (rbf_eval_host_loop) into a pinned host result, queued when the loop
-      runs in a one-cluster shape (it then finishes in the same call);
-      otherwise the two calls one after the other.
+    * ``points`` host (n, 3) array: copied to the device on a side stream while
+      the loop runs (pageable arrays staged through pinned memory piece by
+      piece), then chunked kernels + result copies (rbf_eval_host_loop) into
+      a pinned host result -- when the loop runs in a one-cluster shape (it
+      then finishes in the same call); otherwise the two calls one after the
+      other.
 
     Returns (SelectionResult, moved). Bitwise the values of the two calls."""
     from .core import _PIPELINE_CHUNKS, _device, deform_points
@@ -706,7 +708,7 @@ def select_and_deform(boundary, config, points, out=None):
         res = gcb_select(boundary, config)
         return res, (out if on_device else out.numpy())
 
-    staged = [None]
+    uploaded = [None]
 
     def then(buf, mode):
         if on_device:
@@ -717,17 +719,30 @@ def select_and_deform(boundary, config, points, out=None):
             return True
         if mode not in (N.GCB_MSG, N.GCB_SMEM):
             return False  # a GRID run pauses for capacity: the copies would be wasted
-        src = pts
-        if not src.is_pinned():
-            # pageable input: staged into pinned memory by the host while the
-            # loop runs on the device (torch's multi-threaded copy), so the
-            # pipeline's copies are asynchronous DMA
-            if staged[0] is None:
-                staged[0] = t.empty(pts.shape, dtype=t.float64, pin_memory=True)
-                staged[0].copy_(pts)
-            src = staged[0]
+        if uploaded[0] is None:
+            # the volume goes to the device on a side stream WHILE the loop
+            # runs (a concurrent 48 MB copy slows the one-cluster loop by
+            # ~1 %, tools/dma_interference.py); a pageable array is staged
+            # into pinned memory by the host in pieces, each piece's copy
+            # issued as soon as it is staged
+            side = t.cuda.Stream()
+            if pts.is_pinned():
+                with t.cuda.stream(side):
+                    dev_in.copy_(pts, non_blocking=True)
+            else:
+                staged = t.empty(pts.shape, dtype=t.float64, pin_memory=True)
+                step = max(1, -(-n // 4))
+                for lo in range(0, n, step):
+                    staged[lo:lo + step].copy_(pts[lo:lo + step])
+                    with t.cuda.stream(side):
+                        dev_in[lo:lo + step].copy_(staged[lo:lo + step], non_blocking=True)
+                uploaded.append(staged)  # keep the staging buffer alive until the copies ran
+            ev = t.cuda.Event()
+            ev.record(side)
+            uploaded[0] = ev
+        t.cuda.current_stream().wait_event(uploaded[0])
         with N.launching("rbf_eval", kernels=_PIPELINE_CHUNKS):
-            rc = lib.rbf_eval_host_loop(src.data_ptr(), n, buf.sup.data_ptr(), buf.cap, buf.state.data_ptr(),
+            rc = lib.rbf_eval_host_loop(None, n, buf.sup.data_ptr(), buf.cap, buf.state.data_ptr(),
                                         float(config.radius), 1, N.dptr(dev_in), N.dptr(dev_out),
                                         out.data_ptr(), _PIPELINE_CHUNKS, N.stream_ptr())
         N.check(rc, "rbf_eval_host_loop")
