@@ -748,7 +748,11 @@ def select_and_deform(boundary, config, points, out=None):
         N.check(rc, "rbf_eval_host_loop")
         return True
 
-    res = _gcb_run(boundary, config, then=then)
+    try:
+        res = _gcb_run(boundary, config, then=then)
+    except BaseException:
+        t.cuda.synchronize()  # copies queued on the side stream still read our buffers
+        raise
     if not getattr(res, "_then_done", False):  # the loop finished in a round without it
         if on_device:
             from .core import eval_device
