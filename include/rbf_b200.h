@@ -79,6 +79,8 @@ RBF_API int rbf_eval(const double* targets, int64_t n_targets,
  * pieces overlap (PCIe is full duplex). Results land in `host_out` (pinned
  * memory for asynchronous copies) once `stream` is synchronised; bitwise
  * equal to rbf_eval on the whole array. Support arrays are device pointers.
+ * host_targets == NULL: the targets are already in dev_in (copied there
+ * ahead of time in stream order); only the kernels and result copies run.
  */
 RBF_API int rbf_eval_host(const double* host_targets, int64_t n_targets,
                   const double* sup_points, const double* sup_weights, int64_t n_sup,

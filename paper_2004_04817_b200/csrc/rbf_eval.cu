@@ -476,7 +476,7 @@ extern "C" int rbf_eval_host(const double* host_targets, int64_t n_targets, cons
   if (n_targets < 0 || n_sup < 0) return set_error(RBF_EARG, "negative size");
   if (!(radius > 0.0)) return set_error(RBF_EARG, "radius must be positive, got %g", radius);
   if (n_targets == 0) return RBF_OK;
-  if (!host_targets || !host_out || !dev_in || !dev_out || (n_sup > 0 && (!sup_points || !sup_weights)))
+  if (!host_out || !dev_in || !dev_out || (n_sup > 0 && (!sup_points || !sup_weights)))
     return set_error(RBF_EARG, "null pointer");
   return eval_pipeline(host_targets, n_targets, dev_in, dev_out, host_out, chunks, stream,
                        [&](const double* in, int64_t cnt, double* out, cudaStream_t cs) {

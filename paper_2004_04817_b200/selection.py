@@ -710,6 +710,38 @@ def select_and_deform(boundary, config, points, out=None):
 
     uploaded = [None]
 
+    def upload():
+        """The volume to the device on a side stream while the loop runs (a
+        concurrent 48 MB copy slows the one-cluster loop by ~1 %,
+        tools/dma_interference.py); a pageable array is staged into pinned
+        memory by the host in pieces, each piece's copy issued as soon as it is
+        staged. Once per call; the fallback below reuses the copy."""
+        if uploaded[0] is not None:
+            return
+        side = t.cuda.Stream()
+        if pts.is_pinned():
+            with t.cuda.stream(side):
+                dev_in.copy_(pts, non_blocking=True)
+        else:
+            staged = t.empty(pts.shape, dtype=t.float64, pin_memory=True)
+            step = max(1, -(-n // 4))
+            for lo in range(0, n, step):
+                staged[lo:lo + step].copy_(pts[lo:lo + step])
+                with t.cuda.stream(side):
+                    dev_in[lo:lo + step].copy_(staged[lo:lo + step], non_blocking=True)
+            uploaded.append(staged)  # keep the staging buffer alive until the copies ran
+        ev = t.cuda.Event()
+        ev.record(side)
+        uploaded[0] = ev
+
+    # the result copies of a round that does not finish the loop are wasted
+    # (and the caller's stream waits for them): queue the pipeline in a
+    # one-cluster round only when that shape can run to its capacity without
+    # handing over to the grid for large scans (card * 383 <= 4e5 pairs,
+    # rbf_gcb.cu kClusterScanPairs) -- configs[0-1], not configs[2]
+    card_max = -(-len(boundary) // config.m)
+    queue_pipeline = card_max * 383 <= 400_000
+
     def then(buf, mode):
         if on_device:
             with N.launching("rbf_eval", kernels=1):
@@ -717,29 +749,9 @@ def select_and_deform(boundary, config, points, out=None):
                                        float(config.radius), 1, N.dptr(out), N.stream_ptr())
             N.check(rc, "rbf_eval_loop")
             return True
-        if mode not in (N.GCB_MSG, N.GCB_SMEM):
-            return False  # a GRID run pauses for capacity: the copies would be wasted
-        if uploaded[0] is None:
-            # the volume goes to the device on a side stream WHILE the loop
-            # runs (a concurrent 48 MB copy slows the one-cluster loop by
-            # ~1 %, tools/dma_interference.py); a pageable array is staged
-            # into pinned memory by the host in pieces, each piece's copy
-            # issued as soon as it is staged
-            side = t.cuda.Stream()
-            if pts.is_pinned():
-                with t.cuda.stream(side):
-                    dev_in.copy_(pts, non_blocking=True)
-            else:
-                staged = t.empty(pts.shape, dtype=t.float64, pin_memory=True)
-                step = max(1, -(-n // 4))
-                for lo in range(0, n, step):
-                    staged[lo:lo + step].copy_(pts[lo:lo + step])
-                    with t.cuda.stream(side):
-                        dev_in[lo:lo + step].copy_(staged[lo:lo + step], non_blocking=True)
-                uploaded.append(staged)  # keep the staging buffer alive until the copies ran
-            ev = t.cuda.Event()
-            ev.record(side)
-            uploaded[0] = ev
+        upload()
+        if mode not in (N.GCB_MSG, N.GCB_SMEM) or not queue_pipeline:
+            return False  # this round may not finish the loop: no result copies yet
         t.cuda.current_stream().wait_event(uploaded[0])
         with N.launching("rbf_eval", kernels=_PIPELINE_CHUNKS):
             rc = lib.rbf_eval_host_loop(None, n, buf.sup.data_ptr(), buf.cap, buf.state.data_ptr(),
@@ -761,7 +773,19 @@ def select_and_deform(boundary, config, points, out=None):
             sw = t.from_numpy(np.ascontiguousarray(res.support.weights)).to(pts.device)
             eval_device(pts, sp, sw, config.radius, deform=True, out=out)
             return res, out
-        return res, deform_points(host, res.support, config.radius)
+        if uploaded[0] is None:
+            return res, deform_points(host, res.support, config.radius)
+        # the volume is on the device already: kernels + result copies only
+        t.cuda.current_stream().wait_event(uploaded[0])
+        sp = t.from_numpy(np.ascontiguousarray(res.support.points)).to(dev_in.device)
+        sw = t.from_numpy(np.ascontiguousarray(res.support.weights)).to(dev_in.device)
+        with N.launching("rbf_eval", kernels=_PIPELINE_CHUNKS):
+            rc = lib.rbf_eval_host(None, n, N.dptr(sp), N.dptr(sw), sp.shape[0], float(config.radius), 1,
+                                   N.dptr(dev_in), N.dptr(dev_out), out.data_ptr(), _PIPELINE_CHUNKS,
+                                   N.stream_ptr())
+        N.check(rc, "rbf_eval_host")
+        t.cuda.current_stream().synchronize()
+        return res, out.numpy()
     if on_device:
         return res, out
     t.cuda.current_stream().synchronize()
