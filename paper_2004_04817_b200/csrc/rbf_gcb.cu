@@ -69,7 +69,10 @@ constexpr int kFlagTailOnly = 1 << 17;   // that tail launch: final sweep of a f
 // one-cluster paths: after this many consecutive groups within tolerance
 // (and m >= 2x it) the rest of the run is resolved by the tail launch from
 // one whole-boundary pass (the weights do not change until an append)
-constexpr int kStreakHandover = 8;
+#ifndef RBF_STREAK_HANDOVER
+#define RBF_STREAK_HANDOVER 8
+#endif
+constexpr int kStreakHandover = RBF_STREAK_HANDOVER;
 constexpr int kFlagResumeOnly = 1 << 18;  // a second one-cluster launch queued behind the tail:
                                           // runs only if the state asks to resume in its shape
 
