@@ -30,8 +30,9 @@ print(best)
 args = sys.argv[1:]
 NV = int(args[args.index("--nv") + 1]) if "--nv" in args else 2_000_000
 NC = int(args[args.index("--nc") + 1]) if "--nc" in args else 287
+variants = [int(a) for a in args if a.isdigit() and (args.index(a) == 0 or args[args.index(a) - 1] not in ("--nv", "--nc"))]
 res = {}
-for v in range(12):
+for v in variants or range(13):
     env = dict(os.environ, RBF_EVAL_VARIANT=str(v))
     r = subprocess.run([sys.executable, "-c", CODE, str(NV), str(NC)], env=env, capture_output=True, text=True)
     ms = float(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else None
