@@ -32,6 +32,9 @@
 
 #include <cmath>
 #include <cstdint>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "rbf_common.cuh"
 #include "rbf_internal.h"
@@ -2682,6 +2685,23 @@ __global__ void __launch_bounds__(kLoopThreads, 1) gcb_msg_kernel(rbf_gcb_args a
   P.tmem_free();
 }
 
+// Kernel attributes (dynamic shared memory, non-portable cluster size) are
+// per function and device: set them once per process instead of on every
+// launch (a host call each, on the path before the first loop launch).
+static cudaError_t func_attrs_once(const void* fn, size_t smem, bool cluster) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({fn, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess && cluster) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess) done.insert({fn, dev});
+  return e;
+}
+
 // The whole-GPU launch queued behind a one-cluster launch: the final sweep of
 // a finished loop, or the resolution of a run of groups within tolerance
 // (gcb_driver); it returns at once otherwise.
@@ -2691,7 +2711,7 @@ static cudaError_t launch_tail(const rbf_gcb_args& a, LoopScratch& s, int ctas, 
   t.mode = RBF_GCB_GRID;
   const size_t smem = sizeof(GlobalShared);
   auto grid_kernel = ph ? gcb_grid_kernel<true> : gcb_grid_kernel<false>;
-  cudaError_t e = cudaFuncSetAttribute(grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = func_attrs_once((const void*)grid_kernel, smem, false);
   if (e != cudaSuccess) return e;
   cudaLaunchAttribute at;
   at.id = cudaLaunchAttributeCooperative;
@@ -2714,9 +2734,7 @@ static int resolve_mode(int mode, int nb, int m) {
 
 static cudaError_t launch_cluster(const void* fn, rbf_gcb_args& a, LoopScratch& s, size_t smem,
                                   cudaStream_t st, int nclusters = 1) {
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaError_t e = func_attrs_once(fn, smem, true);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kClusterCTAs * nclusters);
@@ -2846,7 +2864,7 @@ extern "C" int rbf_gcb_run(const rbf_gcb_args* args, void* stream) {
   } else {
     const size_t smem = sizeof(GlobalShared);
     auto grid_kernel = ph ? gcb_grid_kernel<true> : gcb_grid_kernel<false>;
-    RBF_CUDA_TRY(cudaFuncSetAttribute(grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RBF_CUDA_TRY(func_attrs_once((const void*)grid_kernel, smem, false));
     // Li is read twice per append (c0 = Li row, c = c0 + Li r): keep its first
     // persisting-L2 share resident (an access-policy window on this launch),
     // while L and the column copy stream from HBM. rbf_l2_release() returns
