@@ -239,6 +239,8 @@ typedef struct rbf_gcb_state {
 #define RBF_GCB_NO_SWEEP 8   /* end the loop without the final sweep (state->final_pos = -1,
                                 no final record): the caller sweeps the boundary itself, e.g.
                                 sharded over GPUs with rbf_errors_argmax_dev + rbf_best_fold */
+#define RBF_GCB_REFINE 16    /* MSG path: the refinement step in every append (by default it
+                                starts once min l_i^2 < 1e-7; A/B tests) */
 
 /* Launch shapes of the selection kernel:
  *  MSG     one 16-CTA cluster, n < 384: the factor rows (owner-stable, row

@@ -28,6 +28,7 @@ GCB_PHASES = 1  # rbf_gcb_args.flags: record per-phase SM cycles
 GCB_NO_OVERLAP = 2  # rbf_gcb_args.flags: MSG path without the overlapped next-group scan
 GCB_NO_TAIL = 4  # rbf_gcb_args.flags: one-cluster final sweep without the whole-GPU tail launch
 GCB_NO_SWEEP = 8  # rbf_gcb_args.flags: end the loop without the final sweep (the caller sweeps)
+GCB_REFINE = 16  # rbf_gcb_args.flags: MSG path refines every append (default: once min l_i^2 < 1e-7)
 STATUS_DONE = 1
 GCB_AUTO = 0
 GCB_CLUSTER = 1

@@ -76,6 +76,15 @@ constexpr int kFlagTailOnly = 1 << 17;   // that tail launch: final sweep of a f
 #define RBF_STREAK_HANDOVER 8
 #endif
 constexpr int kStreakHandover = RBF_STREAK_HANDOVER;
+// MSG path: the append's refinement step (r = row - L c0, c = c0 + Li r)
+// runs once the smallest pivot^2 so far (min l_i^2) drops below this; above
+// it the factor is well enough conditioned that c = Li row alone keeps the
+// weights within ~3e-10 of the reference's, and the append
+// saves two of its dependent DSMEM hops. 0 = always refine.
+#ifndef RBF_REFINE_BELOW_P2
+#define RBF_REFINE_BELOW_P2 1e-7
+#endif
+constexpr double kRefineBelowP2 = RBF_REFINE_BELOW_P2;
 constexpr int kFlagResumeOnly = 1 << 18;  // a second one-cluster launch queued behind the tail:
                                           // runs only if the state asks to resume in its shape
 
@@ -1389,6 +1398,14 @@ struct MsgPath {
   __device__ static constexpr int best_cache_cap() { return 0; }
   __device__ Common& cm() { return sh.cm; }
   unsigned gathers;  // publications so far (cross-cluster sequence numbers)
+  double min_p2 = 1.0;  // min over the factor's l_i * l_i (identical in every thread)
+  __device__ bool refine() const { return (a.flags & RBF_GCB_REFINE) || !(min_p2 >= kRefineBelowP2); }
+  __device__ void note_pivot(int res, double p2) {
+    if (res == kAccepted) {
+      const double l = sqrt(p2);
+      min_p2 = fmin(min_p2, l * l);
+    }
+  }
   __device__ int rank() const { return blockIdx.x % kClusterCTAs; }
   __device__ int cluster() const { return blockIdx.x / kClusterCTAs; }
   __device__ int nclusters() const { return gridDim.x / kClusterCTAs; }
@@ -1484,6 +1501,20 @@ struct MsgPath {
       for (int r = i + threadIdx.x; r < n; r += kLoopThreads) sh.Licol[oc + (r - i)] = __ldcg(a.Li + tri_off(r) + i);
     }
     for (int g = threadIdx.x; g <= a.m && g <= kMsgGoff; g += kLoopThreads) sh.goff[g] = __ldg(a.group_off + g);
+    // min l_i^2 of the rows already factored (a resumed run decides its
+    // refinements exactly as an uninterrupted one: note_pivot squares the
+    // same stored l)
+    double mp = 1.0;
+    for (int i = threadIdx.x; i < n; i += kLoopThreads) {
+      const double l = __ldcg(a.L + tri_off(i) + i);
+      mp = fmin(mp, l * l);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mp = fmin(mp, __shfl_xor_sync(0xffffffffu, mp, off));
+    if ((threadIdx.x & 31) == 0) sh.cm.wred[threadIdx.x >> 5][0] = mp;
+    __syncthreads();
+    min_p2 = 1.0;
+    for (int w = 0; w < kLoopWarps; ++w) min_p2 = fmin(min_p2, sh.cm.wred[w][0]);
     __syncthreads();
   }
   __device__ void finish() { sync(); }
@@ -1941,10 +1972,13 @@ struct MsgPath {
     n = sh.ov_n;
     phase_bits = sh.ov_bits;  // the scan warps skipped the append's waits
     *pivot2_out = sh.cm.dbl[5];
+    note_pivot(res, *pivot2_out);
     return res;
   }
   __device__ int append(int pos, int& n, bool check_dup, double* pivot2_out) {
-    return append_t<false>(pos, n, check_dup, pivot2_out);
+    const int res = append_t<false>(pos, n, check_dup, pivot2_out);
+    note_pivot(res, *pivot2_out);
+    return res;
   }
 
   // ------------------------------------------------------------------ append
@@ -2033,40 +2067,45 @@ struct MsgPath {
       return kRejectDup;
     }
     pc.mark(1);
-    // c0 = Li row
-    expect(kMbC0, n * 8);
-    for_owned_row_pairs<kWA>(n, [&](int qa, int ia, int qb, int ib) {
-      double va, vb;
-      own_dot2(sh.Liown, qa, ia, qb, ib, [&](int j) { return sh.row[j]; }, lane, va, vb);
-      bcast(sh.c0, ia, va, kMbC0, lane);
-      if (qb >= 0) bcast(sh.c0, ib, vb, kMbC0, lane);
-    });
-    wait(kMbC0);
-    pc.mark(2);
-    // r = row - L c0
-    expect(kMbR, n * 8);
-    for_owned_row_pairs<kWA>(n, [&](int qa, int ia, int qb, int ib) {
-      double va, vb;
-      own_dot2(sh.Lown, qa, ia, qb, ib, [&](int j) { return sh.c0[j]; }, lane, va, vb);
-      bcast(sh.r, ia, sh.row[ia] - va, kMbR, lane);
-      if (qb >= 0) bcast(sh.r, ib, sh.row[ib] - vb, kMbR, lane);
-    });
-    wait(kMbR);
+    const bool ref = refine();
+    if (ref) {
+      // c0 = Li row
+      expect(kMbC0, n * 8);
+      for_owned_row_pairs<kWA>(n, [&](int qa, int ia, int qb, int ib) {
+        double va, vb;
+        own_dot2(sh.Liown, qa, ia, qb, ib, [&](int j) { return sh.row[j]; }, lane, va, vb);
+        bcast(sh.c0, ia, va, kMbC0, lane);
+        if (qb >= 0) bcast(sh.c0, ib, vb, kMbC0, lane);
+      });
+      wait(kMbC0);
+      pc.mark(2);
+      // r = row - L c0
+      expect(kMbR, n * 8);
+      for_owned_row_pairs<kWA>(n, [&](int qa, int ia, int qb, int ib) {
+        double va, vb;
+        own_dot2(sh.Lown, qa, ia, qb, ib, [&](int j) { return sh.c0[j]; }, lane, va, vb);
+        bcast(sh.r, ia, sh.row[ia] - va, kMbR, lane);
+        if (qb >= 0) bcast(sh.r, ib, sh.row[ib] - vb, kMbR, lane);
+      });
+      wait(kMbR);
+    }
     pc.mark(3);
-    // c = c0 + Li r, partial sums of c.c and c.y over the owned rows
+    // c = c0 + Li r (refined) or c = Li row, partial sums of c.c and c.y over
+    // the owned rows
     expect(kMbC1, n * 8 + kClusterCTAs * 32);
     double pcc = 0.0, pcy0 = 0.0, pcy1 = 0.0, pcy2 = 0.0;
+    const double* xv = ref ? sh.r : sh.row;
     for_owned_row_pairs<kWA>(n, [&](int qa, int ia, int qb, int ib) {
       double va, vb;
-      own_dot2(sh.Liown, qa, ia, qb, ib, [&](int j) { return sh.r[j]; }, lane, va, vb);
-      const double ca = sh.c0[ia] + va;
+      own_dot2(sh.Liown, qa, ia, qb, ib, [&](int j) { return xv[j]; }, lane, va, vb);
+      const double ca = ref ? sh.c0[ia] + va : va;
       bcast(sh.c1, ia, ca, kMbC1, lane);
       pcc = fma(ca, ca, pcc);
       pcy0 = fma(ca, sh.y0[ia], pcy0);
       pcy1 = fma(ca, sh.y1[ia], pcy1);
       pcy2 = fma(ca, sh.y2[ia], pcy2);
       if (qb >= 0) {
-        const double cb = sh.c0[ib] + vb;
+        const double cb = ref ? sh.c0[ib] + vb : vb;
         bcast(sh.c1, ib, cb, kMbC1, lane);
         pcc = fma(cb, cb, pcc);
         pcy0 = fma(cb, sh.y0[ib], pcy0);

@@ -565,6 +565,8 @@ def _gcb_run(boundary, config, mode=None, phases=None, sweep=True, then=None):
         args.flags |= N.GCB_NO_OVERLAP
     if os.environ.get("RBF_GCB_TAIL", "1") == "0":  # A/B: final sweep inside the one-cluster launch
         args.flags |= N.GCB_NO_TAIL
+    if os.environ.get("RBF_GCB_REFINE", "") == "1":  # A/B: MSG appends always refined
+        args.flags |= N.GCB_REFINE
     if not sweep:
         args.flags |= N.GCB_NO_SWEEP
     args.radius = radius

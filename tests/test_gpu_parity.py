@@ -589,6 +589,31 @@ def test_selection_overlapped_scan_on_off(cuda, monkeypatch, name):
     assert np.abs(lm["1"] - lm["0"]).max() <= 1e-12 * lm["0"].max()
 
 
+@pytest.mark.parametrize("name", ["cfg1_m32", "cfg0_m1", "hemisphere_m4"])
+def test_selection_refinement_conditional_and_always(cuda, monkeypatch, name):
+    """MSG appends refine c only once min l_i^2 < 1e-7 (default) or always
+    (RBF_GCB_REFINE=1): both reproduce the reference's
+    sequence and records with weights within 1e-9, and their per-record
+    maxima agree to rounding."""
+    from paper_2004_04817_b200 import _native as N
+    from paper_2004_04817_b200.selection import _gcb_run
+
+    g = load_golden(name)
+    pts, disp, _ = golden_inputs(name, g)
+    radius, tol, cap, m, seed = g["params"]
+    b = cuda.BoundarySet(np.arange(len(pts)), pts, disp)
+    cfg = cuda.SelectionConfig(radius=radius, tol=tol, max_supports=int(cap), m=int(m), seed=int(seed))
+    lm = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("RBF_GCB_REFINE", flag)
+        res = _gcb_run(b, cfg, mode=N.GCB_MSG)
+        assert np.array_equal(res.support.nodes, g["seq"]), flag
+        assert [r.node for r in res.history.records] == g["rec_node"].tolist(), flag
+        assert rel(res.support.weights, g["weights"]) <= 1e-9, flag
+        lm[flag] = np.array([r.local_max_error for r in res.history.records])
+    assert np.abs(lm["1"] - lm["0"]).max() <= 1e-9 * lm["0"].max()
+
+
 @pytest.mark.parametrize("name", ["cfg1_m32", "cfg0_m8", "smooth3_m5"])
 @pytest.mark.parametrize("mode", ["msg", "smem"])
 def test_selection_tail_sweep_on_off(cuda, monkeypatch, name, mode):
