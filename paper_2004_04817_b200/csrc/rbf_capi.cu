@@ -127,18 +127,34 @@ extern "C" int rbf_partition(uint64_t state_hi, uint64_t state_lo, uint64_t inc_
   g.inc = ((unsigned __int128)inc_hi << 64) | inc_lo;
   int32_t* perm = new int32_t[nb];
   for (int64_t i = 0; i < nb; ++i) perm[i] = (int32_t)i;
-  for (int64_t i = nb - 1; i >= 1; --i) {
-    const int64_t j = (int64_t)g.interval((uint64_t)i);
+  // Fisher-Yates from the top. The masked rejection loop of
+  // random_interval() is walked draw by draw without a data-dependent branch:
+  // a rejected draw swaps perm[i] with itself and leaves i where it is (the
+  // accept/reject branch mispredicts on ~1 draw in 4 otherwise).
+  // (nb <= INT32_MAX: every bound takes the 32-bit draws.)
+  for (int64_t i = nb - 1; i >= 1;) {
+    const uint64_t mask = ~0ull >> __builtin_clzll((uint64_t)i);
+    const uint64_t v = g.next32() & mask;
+    const bool take = v <= (uint64_t)i;
+    const int64_t j = take ? (int64_t)v : i;
     const int32_t t = perm[j];
     perm[j] = perm[i];
     perm[i] = t;
+    i -= take;
   }
+  // group j = perm[j::m]: sizes are known, so one sequential pass over perm
+  // deals it into the m groups (a strided read per group misses the cache
+  // on every element once nb * 4 B outgrows L1)
   int64_t o = 0;
   for (int64_t j = 0; j < m; ++j) {
     group_off_host[j] = (int32_t)o;
-    for (int64_t i = j; i < nb; i += m) group_pos_host[o++] = perm[i];
+    o += nb / m + (j < nb % m ? 1 : 0);
   }
   group_off_host[m] = (int32_t)o;
+  for (int64_t base = 0, q = 0; base < nb; base += m, ++q) {
+    const int64_t cnt = nb - base < m ? nb - base : m;
+    for (int64_t j = 0; j < cnt; ++j) group_pos_host[group_off_host[j] + q] = perm[base + j];
+  }
   delete[] perm;
   return RBF_OK;
 }

@@ -40,11 +40,14 @@ __device__ __forceinline__ double rsqrt_approx(double x) {
   return y;
 }
 
-// max(t, +0) through the sign bit: integer ops only, keeps the FP64 pipe free
+// max(t, 0) for the Wendland factor in ONE integer instruction: a negative t
+// has a negative high word, which max(hi, 0) replaces by 0 while the low word
+// stays -- the result is a subnormal (< 2^-1042), whose square underflows to
+// exactly +0, so phi = t^4 (5 - 4t) = 0 exactly as with a full clamp. (Every
+// non-FP64 instruction costs an issue slot the FP64 pipe then idles for:
+// measured 2 x FP64 + 1 x other issue cycles per pair.)
 __device__ __forceinline__ double clamp_nonneg(double t) {
-  const int hi = __double2hiint(t), lo = __double2loint(t);
-  const int keep = ~(hi >> 31);
-  return __hiloint2double(hi & keep, lo & keep);
+  return __hiloint2double(max(__double2hiint(t), 0), __double2loint(t));
 }
 
 // t = 1 - eta from r2 = eta^2 in 5 FP64 instructions. y0 = MUFU.RSQ64H(r2)
@@ -54,13 +57,22 @@ __device__ __forceinline__ double clamp_nonneg(double t) {
 // a third-order correction (truncation ~2^-62) written as two nested FMAs:
 // |t - (1 - sqrt(r2))| <= 2.8e-16 over r2 in [1e-10, 1.2] (pair_lab), the
 // same ulp-level error as the 6-instruction rsqrt refinement it replaces.
-__device__ __forceinline__ double t_from_r2(double r2) {
-  const double y0 = rsqrt_approx(r2);
+__device__ __forceinline__ double t_from_seed(double r2, double y0) {
   const double eta0 = r2 * y0;
   const double e = fma(-eta0, y0, 1.0);
   const double p = fma(e, 0.375, 0.5);
   const double w = fma(e, p, 1.0);
   return fma(-eta0, w, 1.0);
+}
+
+__device__ __forceinline__ double t_from_r2(double r2) { return t_from_seed(r2, rsqrt_approx(r2)); }
+
+// phi = max(t, 0)^4 (5 - 4t) from r2 and its rsqrt seed y0 = MUFU.RSQ64H(r2)
+__device__ __forceinline__ double phi_from_seed(double r2, double y0) {
+  double t = clamp_nonneg(t_from_seed(r2, y0));
+  const double q = fma(-4.0, t, 5.0);
+  t = t * t;
+  return (t * t) * q;
 }
 
 // Throughput pair: target (px,py,pz) and support (sx,sy,sz) already scaled
@@ -69,20 +81,21 @@ __device__ __forceinline__ double t_from_r2(double r2) {
 //
 // FP64-pipe budget per pair: 3 DADD (differences) + 3 (r^2) + 5 (t = 1 - eta)
 // + 4 (q = 5 - 4t = 4 eta + 1, t^2, t^4, t^4 q) + 3 DFMA (accumulate) = 18.
-// t_from_r2() never forms sqrt(r2) separately; see there. r2 below 1e-200 is
-// lifted to 1e-200 (eta = 1e-100 gives phi = 1 exactly, like eta = 0) so the
-// rsqrt never sees zero. The clamp t = max(t, 0) is integer-only.
+// t_from_r2() never forms sqrt(r2) separately; see there. r2 carries a 1e-200
+// addend (eta = 1e-100 gives phi = 1 exactly, like eta = 0) so the rsqrt never
+// sees zero. The clamp t = max(t, 0) is one integer instruction.
+__device__ __forceinline__ double pair_r2(double px, double py, double pz,
+                                          double sx, double sy, double sz) {
+  const double dx = px - sx, dy = py - sy, dz = pz - sz;
+  // the 1e-200 rides in the first FMA: it vanishes in the rounding of any
+  // r2 > 1e-184 and keeps the rsqrt away from zero for coincident points
+  return fma(dz, dz, fma(dy, dy, fma(dx, dx, 1e-200)));
+}
+
 __device__ __forceinline__ double pair_phi(double px, double py, double pz,
                                            double sx, double sy, double sz) {
-  const double dx = px - sx, dy = py - sy, dz = pz - sz;
-  double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-  const int kTinyHi = 0x16687e92;  // high word of 1e-200
-  const int hi = __double2hiint(r2);
-  r2 = __hiloint2double(max(hi, kTinyHi), __double2loint(r2));
-  double t = clamp_nonneg(t_from_r2(r2));
-  const double q = fma(-4.0, t, 5.0);
-  t = t * t;
-  return (t * t) * q;
+  const double r2 = pair_r2(px, py, pz, sx, sy, sz);
+  return phi_from_seed(r2, rsqrt_approx(r2));
 }
 
 __device__ __forceinline__ void pair_accum(double px, double py, double pz,
@@ -90,32 +103,6 @@ __device__ __forceinline__ void pair_accum(double px, double py, double pz,
                                            double wx, double wy, double wz,
                                            double& ax, double& ay, double& az) {
   const double f = pair_phi(px, py, pz, sx, sy, sz);
-  ax = fma(wx, f, ax);
-  ay = fma(wy, f, ay);
-  az = fma(wz, f, az);
-}
-
-// Volume-evaluation pair in expanded form. Coordinates are taken relative
-// to an origin o (the first support) and scaled by 1/R; per target
-// P = |p'|^2, per support (-2 s', S = |s'|^2) are precomputed, so
-//   r^2 = (P + S) + p'.(-2 s')            (1 DADD + 3 DFMA instead of 6)
-// and the pair costs 16 FP64-pipe instructions. Absolute error of r^2 is
-// ~4u(|p'| + |s'|)^2 (u = 2^-53) and dphi/d(r^2) = -10(1 - eta)^3 is
-// bounded, so phi moves by < 1e-13 on these domains (displacements agree
-// with the reference to ~1e-12 relative; tests/test_gpu_parity.py). Negative
-// or tiny r^2 (coincident points) is lifted to 1e-200 (phi = 1).
-__device__ __forceinline__ void pair_accum_expanded(double px, double py, double pz, double P,
-                                                    double sx2, double sy2, double sz2, double S,
-                                                    double wx, double wy, double wz,
-                                                    double& ax, double& ay, double& az) {
-  double r2 = fma(pz, sz2, fma(py, sy2, fma(px, sx2, P + S)));
-  const int kTinyHi = 0x16687e92;  // high word of 1e-200
-  const int hi = __double2hiint(r2);
-  r2 = __hiloint2double(max(hi, kTinyHi), __double2loint(r2));
-  double t = clamp_nonneg(t_from_r2(r2));
-  const double q = fma(-4.0, t, 5.0);
-  t = t * t;
-  const double f = (t * t) * q;
   ax = fma(wx, f, ax);
   ay = fma(wy, f, ay);
   az = fma(wz, f, az);

@@ -126,69 +126,6 @@ eval_kernel(const double* __restrict__ tpts, const double* __restrict__ tdisp,
   }
 }
 
-// Volume kernel in expanded form (pair_accum_expanded, 16 FP64 per pair).
-// Origin = the first support, so the result does not depend on how the
-// targets are sharded.
-template <int MODE, int NT, int TPT, int TILE, int MINB>
-__global__ void __launch_bounds__(NT, MINB)
-eval_expanded_kernel(const double* __restrict__ tpts, int64_t nt, const double* __restrict__ spts,
-                     const double* __restrict__ sw, int nsup, double inv_r, double* __restrict__ out) {
-  __shared__ double4 s_a[TILE];  // -2 s'x, -2 s'y, -2 s'z, |s'|^2
-  __shared__ double4 s_b[TILE];  // wx, wy, wz, -
-  const double ox = spts[0], oy = spts[1], oz = spts[2];
-  const int64_t base = (int64_t)blockIdx.x * (NT * TPT) + threadIdx.x;
-  double px[TPT], py[TPT], pz[TPT], pp[TPT], ax[TPT], ay[TPT], az[TPT];
-#pragma unroll
-  for (int k = 0; k < TPT; ++k) {
-    const int64_t r = base + (int64_t)k * NT;
-    double x = 0.0, y = 0.0, z = 0.0;
-    if (r < nt) {
-      x = (tpts[3 * r] - ox) * inv_r;
-      y = (tpts[3 * r + 1] - oy) * inv_r;
-      z = (tpts[3 * r + 2] - oz) * inv_r;
-    }
-    px[k] = x;
-    py[k] = y;
-    pz[k] = z;
-    pp[k] = fma(z, z, fma(y, y, x * x));
-    ax[k] = ay[k] = az[k] = 0.0;
-  }
-  for (int t0 = 0; t0 < nsup; t0 += TILE) {
-    const int cnt = min(TILE, nsup - t0);
-    __syncthreads();
-    for (int j = threadIdx.x; j < cnt; j += NT) {
-      const int g = t0 + j;
-      const double x = (spts[3 * g] - ox) * inv_r, y = (spts[3 * g + 1] - oy) * inv_r,
-                   z = (spts[3 * g + 2] - oz) * inv_r;
-      s_a[j] = make_double4(-2.0 * x, -2.0 * y, -2.0 * z, fma(z, z, fma(y, y, x * x)));
-      s_b[j] = make_double4(sw[3 * g], sw[3 * g + 1], sw[3 * g + 2], 0.0);
-    }
-    __syncthreads();
-#pragma unroll 2
-    for (int j = 0; j < cnt; ++j) {
-      const double4 a = s_a[j];
-      const double4 b = s_b[j];
-#pragma unroll
-      for (int k = 0; k < TPT; ++k)
-        pair_accum_expanded(px[k], py[k], pz[k], pp[k], a.x, a.y, a.z, a.w, b.x, b.y, b.z, ax[k], ay[k], az[k]);
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < TPT; ++k) {
-    const int64_t r = base + (int64_t)k * NT;
-    if (r >= nt) continue;
-    if (MODE == kModeDeform) {
-      out[3 * r] = tpts[3 * r] + ax[k];
-      out[3 * r + 1] = tpts[3 * r + 1] + ay[k];
-      out[3 * r + 2] = tpts[3 * r + 2] + az[k];
-    } else {
-      out[3 * r] = ax[k];
-      out[3 * r + 1] = ay[k];
-      out[3 * r + 2] = az[k];
-    }
-  }
-}
-
 // One block folds the per-block (err, pos) partials in block order.
 __global__ void best_reduce_kernel(const Best* __restrict__ partials, int n, double* __restrict__ result,
                                    int64_t pos_offset) {
@@ -242,13 +179,14 @@ __global__ void best_fold_kernel(const double* __restrict__ recs, int64_t n, dou
   }
 }
 
-// Launch variants of the volume kernel: 0 the expanded pair form (128
-// threads x 6 targets), 1-5 the difference form at several geometries
-// (threads, targets per thread, support tile, min resident blocks), 6 the
-// expanded form at 128 x 4, 7-8 the difference form at 64 x 6 (6 CTAs per
-// SM; support tile 128 / 64), 9 the expanded form at 64 x 6, 10-11 short-grid shapes
-// (128 x 2 and 64 x 4: more CTAs when the targets fill less than one wave). RBF_EVAL_VARIANT selects one for experiments
-// (tools/eval_variants.py).
+// Launch variants of the volume kernel: 1-5 launch geometries (threads,
+// targets per thread, support tile, min resident blocks), 7-8 64 x 6 (6 CTAs
+// per SM; support tile 128 / 64), 10-11 short-grid shapes (128 x 2 and 64 x 4:
+// more CTAs when the targets fill less than one wave). RBF_EVAL_VARIANT
+// selects one for experiments (tools/eval_variants.py). The expanded pair form
+// r^2 = |p|^2 + |s|^2 - 2 p.s (16 instead of 18 FP64 instructions) was removed
+// in round 2: with the one-instruction clamp it is no faster than the
+// difference form (19.3-20.0 vs 19.4 TFLOP/s) and less accurate.
 template <int MODE, int NT, int TPT, int TILE, int MINB>
 static void launch_eval_variant(const double* targets, int64_t n, const double* sp, const double* sw,
                                 int ns, double inv_r, double* out, cudaStream_t s) {
@@ -257,21 +195,10 @@ static void launch_eval_variant(const double* targets, int64_t n, const double* 
       targets, nullptr, nullptr, n, sp, sw, ns, inv_r, out, nullptr);
 }
 
-template <int MODE, int NT, int TPT, int TILE, int MINB>
-static void launch_expanded(const double* targets, int64_t n, const double* sp, const double* sw, int ns,
-                            double inv_r, double* out, cudaStream_t s) {
-  const int64_t nblk = (n + NT * TPT - 1) / (NT * TPT);
-  eval_expanded_kernel<MODE, NT, TPT, TILE, MINB><<<(unsigned)nblk, NT, 0, s>>>(targets, n, sp, sw, ns,
-                                                                             inv_r, out);
-}
-
 template <int MODE>
 static void launch_eval(int variant, const double* t, int64_t n, const double* sp, const double* sw, int ns,
                         double inv_r, double* out, cudaStream_t s) {
-  if (ns == 0 && (variant == 0 || variant == 6 || variant == 9)) variant = 4;  // expanded form needs an origin support
   switch (variant) {
-    case 0: launch_expanded<MODE, 128, 6, 128, 3>(t, n, sp, sw, ns, inv_r, out, s); break;
-    case 6: launch_expanded<MODE, 128, 4, 128, 4>(t, n, sp, sw, ns, inv_r, out, s); break;
     case 1: launch_eval_variant<MODE, 128, 8, 128, 2>(t, n, sp, sw, ns, inv_r, out, s); break;
     case 2: launch_eval_variant<MODE, 256, 4, 256, 2>(t, n, sp, sw, ns, inv_r, out, s); break;
     case 3: launch_eval_variant<MODE, 64, 8, 128, 4>(t, n, sp, sw, ns, inv_r, out, s); break;
@@ -279,16 +206,14 @@ static void launch_eval(int variant, const double* t, int64_t n, const double* s
     case 5: launch_eval_variant<MODE, 128, 4, 256, 4>(t, n, sp, sw, ns, inv_r, out, s); break;
     case 7: launch_eval_variant<MODE, 64, 6, 128, 6>(t, n, sp, sw, ns, inv_r, out, s); break;
     case 8: launch_eval_variant<MODE, 64, 6, 64, 6>(t, n, sp, sw, ns, inv_r, out, s); break;
-    case 9: launch_expanded<MODE, 64, 6, 128, 6>(t, n, sp, sw, ns, inv_r, out, s); break;
     case 10: launch_eval_variant<MODE, 128, 2, 128, 8>(t, n, sp, sw, ns, inv_r, out, s); break;
     case 11: launch_eval_variant<MODE, 64, 4, 128, 6>(t, n, sp, sw, ns, inv_r, out, s); break;
     default: launch_eval_variant<MODE, 128, 4, 128, 4>(t, n, sp, sw, ns, inv_r, out, s); break;
   }
 }
 
-// Default: variant 4, the difference form at 128 threads x 6 targets (17.7
-// FP64 TFLOP/s algorithmic on configs[1] vs 18.3 for the expanded form, whose
-// r^2 error is ~10x larger; measured by tools/eval_variants.py).
+// Default: variant 4, 128 threads x 6 targets, 3 CTAs per SM (19.4 FP64
+// TFLOP/s algorithmic on configs[1]; tools/eval_variants.py).
 static int eval_variant() {
   static int v = [] {
     const char* e = getenv("RBF_EVAL_VARIANT");

@@ -3,7 +3,7 @@ goldens (tests/golden/*.npz: the reference's own weights and displacements),
 one process per RBF_EVAL_VARIANT (read once per process):
 
     RBF_EVAL_VARIANT=4 python tools/eval_form_accuracy.py   # difference form
-    RBF_EVAL_VARIANT=0 python tools/eval_form_accuracy.py   # expanded form
+    RBF_EVAL_VARIANT=7 python tools/eval_form_accuracy.py   # 64 x 6 launch shape
 """
 import os
 import sys
