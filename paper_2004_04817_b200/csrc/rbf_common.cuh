@@ -132,17 +132,24 @@ __device__ __forceinline__ Best best_of(Best a, Best b) {
   return better(b.err, b.pos, a.err, a.pos) ? b : a;
 }
 
+// Warp arg-max in three warp-wide integer reductions (redux.sync) instead of
+// a five-level shuffle butterfly of (double, int) pairs: the error's bit
+// pattern is mapped to an unsigned key that orders like the double (sign bit
+// flipped for err >= 0, all bits inverted for the negative sentinel), its high
+// and low words are maximised in turn, and the lowest position among the
+// lanes holding the maximum wins -- the same (err, lowest pos) result as
+// folding the lanes with better(). Every lane returns the warp's best.
 __device__ __forceinline__ Best warp_best(Best b) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    double e = __shfl_xor_sync(0xffffffffu, b.err, off);
-    int p = __shfl_xor_sync(0xffffffffu, b.pos, off);
-    if (better(e, p, b.err, b.pos)) {
-      b.err = e;
-      b.pos = p;
-    }
-  }
-  return b;
+  const unsigned full = 0xffffffffu;
+  const unsigned hi = (unsigned)__double2hiint(b.err), lo = (unsigned)__double2loint(b.err);
+  const unsigned neg = (unsigned)((int)hi >> 31);
+  const unsigned khi = hi ^ (neg | 0x80000000u), klo = lo ^ neg;
+  const unsigned mhi = __reduce_max_sync(full, khi);
+  const unsigned mlo = __reduce_max_sync(full, khi == mhi ? klo : 0u);
+  const bool top = khi == mhi && klo == mlo;
+  const unsigned mp = __reduce_min_sync(full, top ? (unsigned)b.pos : 0xffffffffu);
+  const unsigned mneg = (mhi & 0x80000000u) ? 0u : 0xffffffffu;
+  return Best{__hiloint2double((int)(mhi ^ (mneg | 0x80000000u)), (int)(mlo ^ mneg)), (int)mp};
 }
 
 __device__ __forceinline__ double warp_sum(double v) {

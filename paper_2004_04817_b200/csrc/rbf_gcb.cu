@@ -842,13 +842,18 @@ __device__ __forceinline__ double warp_reduce_scatter16(double (&v)[16], int lan
 // Both arg-max partials of a CTA in one pass; every lane of warp 0 ends with
 // them. `lanes` = how many low lanes of each warp hold candidates (1..32).
 __device__ __forceinline__ void cta_best2(Common& cm, Best& bu, Best& br, int lanes) {
-  for (int off = 1; off < lanes; off <<= 1) {
-    const double eu = __shfl_xor_sync(0xffffffffu, bu.err, off);
-    const int pu = __shfl_xor_sync(0xffffffffu, bu.pos, off);
-    const double er = __shfl_xor_sync(0xffffffffu, br.err, off);
-    const int pr = __shfl_xor_sync(0xffffffffu, br.pos, off);
-    if (better(eu, pu, bu.err, bu.pos)) bu = Best{eu, pu};
-    if (better(er, pr, br.err, br.pos)) br = Best{er, pr};
+  if (lanes > 4) {  // lanes past `lanes` hold the neutral record: fold the whole warp (3 redux each)
+    bu = warp_best(bu);
+    br = warp_best(br);
+  } else {
+    for (int off = 1; off < lanes; off <<= 1) {
+      const double eu = __shfl_xor_sync(0xffffffffu, bu.err, off);
+      const int pu = __shfl_xor_sync(0xffffffffu, bu.pos, off);
+      const double er = __shfl_xor_sync(0xffffffffu, br.err, off);
+      const int pr = __shfl_xor_sync(0xffffffffu, br.pos, off);
+      if (better(eu, pu, bu.err, bu.pos)) bu = Best{eu, pu};
+      if (better(er, pr, br.err, br.pos)) br = Best{er, pr};
+    }
   }
   if ((threadIdx.x & 31) == 0) {
     cm.wb[threadIdx.x >> 5][0] = bu;
@@ -857,16 +862,8 @@ __device__ __forceinline__ void cta_best2(Common& cm, Best& bu, Best& br, int la
   __syncthreads();
   if (threadIdx.x < 32) {
     const int l = threadIdx.x;
-    bu = l < kLoopWarps ? cm.wb[l][0] : Best{-1.0, kNone};
-    br = l < kLoopWarps ? cm.wb[l][1] : Best{-1.0, kNone};
-    for (int off = 1; off < kLoopWarps; off <<= 1) {
-      const double eu = __shfl_xor_sync(0xffffffffu, bu.err, off);
-      const int pu = __shfl_xor_sync(0xffffffffu, bu.pos, off);
-      const double er = __shfl_xor_sync(0xffffffffu, br.err, off);
-      const int pr = __shfl_xor_sync(0xffffffffu, br.pos, off);
-      if (better(eu, pu, bu.err, bu.pos)) bu = Best{eu, pu};
-      if (better(er, pr, br.err, br.pos)) br = Best{er, pr};
-    }
+    bu = warp_best(l < kLoopWarps ? cm.wb[l][0] : Best{-1.0, kNone});
+    br = warp_best(l < kLoopWarps ? cm.wb[l][1] : Best{-1.0, kNone});
   }
 }
 

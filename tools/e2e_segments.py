@@ -32,7 +32,7 @@ def wrap(mod, name):
     setattr(mod, name, inner)
 
 
-for nm in ("_partition_native", "_partition_device", "_boundary_on_device", "_take_buffers", "_give_buffers"):
+for nm in ("_partition_native", "_partition_device_start", "_boundary_on_device", "_take_buffers", "_give_buffers"):
     wrap(S, nm)
 orig_read = S._LoopBuffers.read_all
 
