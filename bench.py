@@ -523,7 +523,26 @@ def run_ours(args, rank, world, local):
     if sweep_ms:
         kernels.append({"kernel": "rbf_errors_argmax_dev (sharded final sweep, this rank's slice)",
                         "ms": statistics.mean(sweep_ms)})
-    dominant = max((k for k in kernels if "frac" in k), key=lambda k: k["ms"]) if kernels else None
+    if getattr(res.history, "device_mode", None) == "grid":
+        # the grid path's appends stream four packed triangles per append (Li for
+        # c0 and for c, L for r, the column copy for u): 4 * 8 n(n+1)/2 bytes at n
+        # supports; against the measured HBM copy bandwidth (small factors are
+        # L2-resident, so this is the algorithmic rate, not DRAM traffic)
+        t2 = sum(r.t2_s for r in res.history.records)
+        tri_bytes = sum(16.0 * n * (n + 1) for n in range(3, nc))
+        hbm = None
+        try:
+            hbm = json.loads((REPO / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs")
+        except (OSError, ValueError):
+            pass
+        if t2 > 0:
+            ach = tri_bytes / t2 / 1e9
+            kernels.append({"kernel": "gcb_grid_kernel appends (t2: triangle streams)", "ms": t2 * 1e3,
+                            "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                            "frac": ach / hbm if hbm else None,
+                            "bytes_per_append": "16 n (n + 1): four packed triangles (SURVEY 8(d): 8 n^2 = two)",
+                            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else "none"})
+    dominant = max((k for k in kernels if "frac" in k and k["unit"] == "TFLOP/s"), key=lambda k: k["ms"]) if kernels else None
 
     cpu = cpu1 = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
