@@ -15,6 +15,7 @@ scan, t2 = weights update + candidate appends (carried into the next
 record, selection.py:310-316, 357).
 """
 
+import os
 import threading
 from collections import OrderedDict
 from dataclasses import dataclass, field, replace
@@ -263,6 +264,15 @@ _buf_pool = {}               # (device, nb, cap, rec_cap, ctas) -> [_LoopBuffers
 
 
 _part_pool = None  # one worker: the host shuffle runs beside the caller's device set-up
+
+
+def _drop_part_pool():
+    global _part_pool
+    _part_pool = None  # a forked child has no worker thread: it makes its own pool
+
+
+if hasattr(os, "register_at_fork"):
+    os.register_at_fork(after_in_child=_drop_part_pool)
 
 
 def _partition_device_start(nb, m, seed):
