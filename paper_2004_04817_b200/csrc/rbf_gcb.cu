@@ -502,14 +502,19 @@ struct GlobalPath {
     const int S = 1 << lg;
     const int g = tid >> lg, sub = tid & (S - 1);
     const bool active = g < groups;
-    if (tid < rem) {  // prefetch row tid's epilogue operands
+    // row tid's epilogue operands: position and displacement are requested
+    // here, together with the rows' points and (below) the first support
+    // tile, so the three arrive in one L2 round trip; the eligibility byte
+    // (addressed by the position) follows and is not needed before the
+    // epilogue
+    int my_pos = 0;
+    double d0 = 0.0, d1 = 0.0, d2 = 0.0;
+    if (tid < rem) {
       const int tt = t0 + tid;
-      const int pos = gpos ? __ldg(gpos + tt) : tt;
-      const bool elig = !__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + pos);
-      mpos[tid] = elig ? pos : ~pos;
-      md[3 * tid] = __ldcg(gdisp + 3 * (int64_t)tt);
-      md[3 * tid + 1] = __ldcg(gdisp + 3 * (int64_t)tt + 1);
-      md[3 * tid + 2] = __ldcg(gdisp + 3 * (int64_t)tt + 2);
+      my_pos = gpos ? __ldg(gpos + tt) : tt;
+      d0 = __ldcg(gdisp + 3 * (int64_t)tt);
+      d1 = __ldcg(gdisp + 3 * (int64_t)tt + 1);
+      d2 = __ldcg(gdisp + 3 * (int64_t)tt + 2);
     }
     double px[kT], py[kT], pz[kT], ax[kT], ay[kT], az[kT];
 #pragma unroll
@@ -522,9 +527,22 @@ struct GlobalPath {
       pz[q] = ok ? __ldcg(gpt + 3 * (int64_t)t + 2) * inv_r : 0.0;
       ax[q] = ay[q] = az[q] = 0.0;
     }
+    bool first_staged = false;
+    if (n > 0 && (!staged || n > kSupTile)) {
+      stage(0, min(kSupTile, n));
+      staged = true;
+      first_staged = true;
+    }
+    if (tid < rem) {
+      const bool elig = !__ldcg(reinterpret_cast<const unsigned char*>(a.inel) + my_pos);
+      mpos[tid] = elig ? my_pos : ~my_pos;
+      md[3 * tid] = d0;
+      md[3 * tid + 1] = d1;
+      md[3 * tid + 2] = d2;
+    }
     for (int s0 = 0; s0 < n; s0 += kSupTile) {
       const int cnt = min(kSupTile, n - s0);
-      if (!staged || n > kSupTile) {
+      if (!(s0 == 0 && first_staged) && (!staged || n > kSupTile)) {
         stage(s0, cnt);
         staged = true;
       }
