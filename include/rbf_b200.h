@@ -256,7 +256,7 @@ typedef struct rbf_gcb_state {
  * pauses (RBF_EGROW) and names the shape to resume in: MSG -> SMEM when n
  * reaches 383 with group scans of at most 1.5e5 pairs (card * n), else ->
  * GRID; SMEM -> GRID when n reaches 1023; any one-cluster shape -> GRID as
- * soon as a group scan exceeds 4e5 pairs. CLUSTER runs only when forced
+ * soon as a group scan exceeds 8e5 pairs. CLUSTER runs only when forced
  * (DESIGN.md §4.2). */
 enum { RBF_GCB_AUTO = 0, RBF_GCB_CLUSTER = 1, RBF_GCB_GRID = 2, RBF_GCB_SMEM = 3, RBF_GCB_MSG = 4 };
 

@@ -53,8 +53,17 @@ constexpr int kSupTile = 2048;       // GlobalPath: supports staged per scan til
 constexpr int kRowSmemMax = 8192;    // GlobalPath: row held in shared memory below this n
                                      // (beyond it, in global scratch: LoopScratch::rowg)
 constexpr int kSmallMax = 1024;      // SmemPath: supports resident in shared memory
-constexpr int kAutoClusterMaxCard = 2048;
-constexpr int64_t kClusterScanPairs = 400000;  // per group scan, see gcb_driver
+#ifndef RBF_AUTO_CLUSTER_MAX_CARD
+#define RBF_AUTO_CLUSTER_MAX_CARD 2048
+#endif
+constexpr int kAutoClusterMaxCard = RBF_AUTO_CLUSTER_MAX_CARD;
+// (measured, tools/sel_time.py on configs[2], card 1,667: 2.5e5 -> 17.6 ms,
+// 4e5 -> 17.06, 6e5 -> 16.71, 8e5 and above -> 16.68: the one-cluster appends
+// (~4 us) beat the grid's (~11 us at small n) for longer than its scans lose)
+#ifndef RBF_CLUSTER_SCAN_PAIRS
+#define RBF_CLUSTER_SCAN_PAIRS 800000
+#endif
+constexpr int64_t kClusterScanPairs = RBF_CLUSTER_SCAN_PAIRS;  // per group scan, see gcb_driver
 // when the MSG path's resident capacity is reached, scans of more pairs than
 // this go to the grid rather than to the shared-memory cluster path
 // (configs[4] m = 187: 31.0 -> 23.6 ms; tools/greedy_ab.py)

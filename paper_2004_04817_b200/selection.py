@@ -775,9 +775,10 @@ def select_and_deform(boundary, config, points, out=None):
 
     # the result copies of a round that does not finish the loop are wasted
     # (and the caller's stream waits for them): queue the pipeline in a
-    # one-cluster round only when that shape can run to its capacity without
-    # handing over to the grid for large scans (card * 383 <= 4e5 pairs,
-    # rbf_gcb.cu kClusterScanPairs) -- configs[0-1], not configs[2]
+    # one-cluster round only for groups of up to ~1,000 nodes (card * 383 <=
+    # 4e5 pairs) -- configs[0-1], whose runs end within the one-cluster
+    # capacity of 383 supports; larger groups (configs[2]) reach the capacity
+    # and move on to the grid
     card_max = -(-len(boundary) // config.m)
     queue_pipeline = card_max * 383 <= 400_000
 
