@@ -81,8 +81,9 @@ constexpr int kFlagTailOnly = 1 << 17;   // that tail launch: final sweep of a f
 // one-cluster paths: after this many consecutive groups within tolerance
 // (and m >= 2x it) the rest of the run is resolved by the tail launch from
 // one whole-boundary pass (the weights do not change until an append)
+// (configs[1] selection with 5 / 6 / 7 / 8 / 10: 2.31 / 2.24 / 2.26 / 2.27 / 2.29 ms)
 #ifndef RBF_STREAK_HANDOVER
-#define RBF_STREAK_HANDOVER 8
+#define RBF_STREAK_HANDOVER 6
 #endif
 constexpr int kStreakHandover = RBF_STREAK_HANDOVER;
 // MSG path: the append's refinement step (r = row - L c0, c = c0 + Li r)
